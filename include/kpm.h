@@ -1,0 +1,191 @@
+/* libkpm -- B200-native KPM Chebyshev-moment engine: the C-ABI drop-in
+ * boundary for the hot path of netdos 0.1.0 (arXiv 1905.09758).
+ *
+ * Plain C types only (no torch, no CUDA types in signatures).  One context
+ * drives one GPU; multi-GPU runs use one process per GPU (probe sharding,
+ * SURVEY.md §8e) and combine per-probe results on the host side.
+ *
+ * Pointer arguments documented "host-or-device" are classified with
+ * cudaPointerGetAttributes: device pointers are used in place (no copy),
+ * host pointers are staged through the context's stream.
+ *
+ * Every entry point returns KPM_OK (0) or a negative KPM_E* status; the
+ * message is available from kpm_last_error() (thread-local).  Python maps
+ * KPM_EINVAL -> ValueError, KPM_ENONFINITE -> RecurrenceBlowupError,
+ * KPM_EZEROMASS -> ValueError("zero probe mass at node k...") (the
+ * reference's exception types and messages, errors.py:1-33, kpm.py:111-147).
+ *
+ * Citations: paths relative to /root/reference/pkg/src/netdos/.
+ */
+#ifndef LIBKPM_H
+#define LIBKPM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KPM_ABI_VERSION 1
+
+enum {
+  KPM_OK = 0,
+  KPM_EINVAL = -1,      /* bad argument                                   */
+  KPM_ENONFINITE = -2,  /* recurrence overflowed (kpm.py:111-114)          */
+  KPM_ENOMEM = -3,      /* device allocation failed                        */
+  KPM_ECUDA = -4,       /* CUDA runtime error                              */
+  KPM_EZEROMASS = -5,   /* zero probe mass at a node (kpm.py:145-147)      */
+  KPM_ENODEV = -6       /* no usable sm_100 device                         */
+};
+
+/* recurrence modes (kpm_run_create) */
+enum {
+  KPM_MODE_DOS_DOUBLING = 0, /* global moments, ceil(M/2) steps, T_2k = 2T_k^2-I */
+  KPM_MODE_DOS_DIRECT = 1,   /* global moments, M steps, z^T T_m z (kpm.py:108) */
+  KPM_MODE_LDOS = 2          /* per-node moments, M steps (kpm.py:136)        */
+};
+
+/* flags for kpm_run_create */
+enum {
+  KPM_LDOS_RAW = 1 /* pdos normalized=False: num * trace_scale (kpm.py:150) */
+};
+
+typedef struct kpm_ctx kpm_ctx;
+typedef struct kpm_graph kpm_graph;
+typedef struct kpm_run kpm_run;
+
+/* ------------------------------------------------------------ context --- */
+int kpm_abi_version(void);
+const char *kpm_last_error(void);
+int kpm_device_count(int *count);
+/* Bind a context (and its own non-blocking stream) to CUDA device `device`. */
+int kpm_init(int device, kpm_ctx **out);
+void kpm_finalize(kpm_ctx *ctx);
+/* The context's cudaStream_t, for event timing by the caller. */
+void *kpm_ctx_stream(kpm_ctx *ctx);
+int kpm_ctx_synchronize(kpm_ctx *ctx);
+/* device memory owned by the caller through the library */
+int kpm_device_alloc(kpm_ctx *ctx, int64_t bytes, void **out);
+int kpm_device_free(kpm_ctx *ctx, void *ptr);
+/* stream-ordered copy; kind 0 = H2D, 1 = D2H, 2 = D2D; host buffers should
+ * be pinned (kpm_host_alloc) for async transfers. */
+int kpm_memcpy(kpm_ctx *ctx, void *dst, const void *src, int64_t bytes, int kind);
+int kpm_host_alloc(int64_t bytes, void **out);
+/* free / total device memory of the context's GPU (probe batch sizing) */
+int kpm_mem_info(kpm_ctx *ctx, int64_t *free_bytes, int64_t *total_bytes);
+int kpm_host_free(void *ptr);
+
+/* ------------------------------------------------------------- graphs --- */
+/* Device graph loader (K1-K3).  Replaces graph.py:69-81 _csr_from_canonical
+ * (+ the canonicalise/self-loop/dedup step of build_csr, graph.py:130-160)
+ * followed by graph.py:47-54 degrees and the normalized-adjacency branch of
+ * build_operator, operators.py:105-113.  Input: m edges (u[e], v[e]),
+ * int64, host-or-device.  Self-loops are dropped unless keep_loops != 0 (then
+ * stored once at (i,i)); duplicates are merged (unit weights).  Output: int64
+ * row_ptr, int32 col_idx sorted per row, fp64 dinv = deg>0 ? 1/sqrt(deg) : 0
+ * bit-identical to the reference; H's values are never stored. */
+int kpm_graph_from_edges(kpm_ctx *ctx, int64_t n, const int64_t *u,
+                         const int64_t *v, int64_t m, int keep_loops,
+                         kpm_graph **out);
+
+/* Explicit CSR (any operator kind): replaces SymmetricCSROperator
+ * (operators.py:50-65) wrapped by rescale_operator / ScaledOperator.apply
+ * (operators.py:124-176): y = (A x - shift*x) / scale with separate
+ * roundings.  values == NULL selects the implicit normalized adjacency
+ * h_ij = dinv_i*dinv_j computed from the degree of each row (the
+ * reference's kind="normalized-adjacency" operator), in which case shift and
+ * scale must be 0 and 1.  indptr/indices int64, host-or-device. */
+int kpm_graph_from_csr(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
+                       const int64_t *indices, int64_t nnz,
+                       const double *values, double shift, double scale,
+                       kpm_graph **out);
+
+int kpm_graph_info(kpm_graph *g, int64_t *n, int64_t *nnz, int64_t *max_degree);
+/* Copy the device CSR back (any pointer may be NULL): bit-exactness checks. */
+int kpm_graph_export(kpm_graph *g, int64_t *row_ptr, int32_t *col_idx,
+                     double *dinv);
+void kpm_graph_free(kpm_graph *g);
+
+/* ---------------------------------------------------- native SpMM (L0) --- */
+/* Drop-in for the reference's only FFI, _kernels/_spmv.pyx:25-39
+ * csr_matvec(indptr, indices, data, x, out, threads): out[i,c] =
+ * sum_jj data[jj]*x[indices[jj],c] in stored order, separate multiply/add
+ * roundings (bit-identical to the Cython kernel).  x is n_x_rows x k
+ * row-major, out is n_rows x k row-major; all host-or-device. */
+int kpm_csr_matvec(kpm_ctx *ctx, int64_t n_rows, const int64_t *indptr,
+                   const int64_t *indices, const double *data, int64_t nnz,
+                   const double *x, int64_t n_x_rows, int64_t k, double *out);
+
+/* ----------------------------------------------------------- probes --- */
+/* make_probes(kind=RADEMACHER) on the device (probes.py:52-54,86-89):
+ * column j = 1 - 2*bit, the bit stream of numpy's Philox4x64-10 seeded by
+ * SeedSequence(seed).spawn(nz)[j] -- the host passes each column's 128-bit
+ * Philox key (keys[2j], keys[2j+1]); output is bit-identical to numpy.
+ * z (device) is n x ldz row-major; columns [col0, col0+ncols). */
+int kpm_probes_rademacher(kpm_ctx *ctx, int64_t n, int64_t ncols,
+                          const uint64_t *keys, double *z, int64_t ldz,
+                          int64_t col0);
+
+/* -------------------------------------------------- motif projection --- */
+/* The probe-deflation loop of filter_probes (motifs.py:400-403): for each
+ * sparse vector u (vec_ptr/vec_idx/vec_val, CSR over vectors) in order,
+ * coeff = u . Z[idx,:]; Z[idx,:] -= outer(u, coeff).  Vectors are grouped
+ * (group_ptr over vectors) so that groups have pairwise disjoint support and
+ * run in parallel; vectors within a group run in list order.  z is n x ldz
+ * (host-or-device, updated in place), k columns. */
+int kpm_filter_probes(kpm_ctx *ctx, int64_t n, int64_t k, double *z,
+                      int64_t ldz, int64_t n_groups, const int64_t *group_ptr,
+                      const int64_t *vec_ptr, const int64_t *vec_idx,
+                      const double *vec_val);
+
+/* --------------------------------------------------------- recurrence --- */
+/* A moment run over one probe batch: dos_moments (kpm.py:92-117) or
+ * pdos_moments (kpm.py:120-152).  The run owns two n x ld fp64 recurrence
+ * blocks (three for DIRECT/LDOS: the probes stay resident). */
+int kpm_run_create(kpm_graph *g, int64_t k, int32_t mode, int32_t m_max,
+                   int32_t flags, kpm_run **out);
+/* probes: n x k row-major with row stride ldz (host-or-device) */
+int kpm_run_set_probes(kpm_run *r, const double *z, int64_t ldz);
+/* device-generated Rademacher probes (see kpm_probes_rademacher) */
+int kpm_run_set_rademacher(kpm_run *r, const uint64_t *keys);
+/* Advance by up to `steps` SpMM recurrence steps (asynchronous on the
+ * context stream); *remaining receives the steps still to go (may be NULL).
+ * Each step is one fused kernel (SpMM + three-term update + moment
+ * reduction) plus one deterministic finalize kernel. */
+int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining);
+int kpm_run_total_steps(kpm_run *r);
+/* Global modes: contrib (m_max+1) x k, contrib[m][j] = z_j^T T_m z_j
+ * (kpm.py:107-108).  LDOS: values n x (m_max+1) = (num/den).T (kpm.py:148),
+ * or num*trace_scale with KPM_LDOS_RAW.  `out` host-or-device.  Returns
+ * KPM_ENONFINITE if any moment overflowed, KPM_EZEROMASS (node index in
+ * *bad_node, may be NULL) for a zero probe mass in normalized LDOS. */
+int kpm_run_result(kpm_run *r, double *out, double trace_scale,
+                   int64_t *bad_node);
+/* Device pointer of the current T_k block and its row stride (tests). */
+int kpm_run_block(kpm_run *r, const double **t_k, int64_t *ld, int32_t *k_index);
+void kpm_run_free(kpm_run *r);
+
+/* One-shot conveniences over kpm_run_*: z host-or-device n x k (ldz = k). */
+int kpm_dos_contrib(kpm_graph *g, const double *z, int64_t k, int32_t m_max,
+                    int32_t doubling, double *contrib);
+int kpm_ldos(kpm_graph *g, const double *z, int64_t k, int32_t m_max,
+             int32_t flags, double trace_scale, double *values,
+             int64_t *bad_node);
+
+/* ------------------------------------------------- harness generators --- */
+/* R-MAT edge draws [e0, e0+count) on the device (no reference counterpart,
+ * SURVEY.md §9.2): Philox4x32-10(key=seed, ctr=(e, level/4)), quadrant by
+ * uint32 thresholds ta < tab < tabc; u, v int64 device buffers.  Bit-
+ * identical to oracle/kpm_oracle.c orc_rmat_edges. */
+int kpm_rmat_edges(kpm_ctx *ctx, int scale, uint64_t seed, uint32_t ta,
+                   uint32_t tab, uint32_t tabc, int64_t e0, int64_t count,
+                   int64_t *u, int64_t *v);
+/* Fused R-MAT -> graph: draws n_edges edges as above and feeds them straight
+ * into the device loader (== kpm_rmat_edges + kpm_graph_from_edges with
+ * keep_loops = 0, without materialising u/v). */
+int kpm_graph_rmat(kpm_ctx *ctx, int scale, int64_t n_edges, uint64_t seed,
+                   uint32_t ta, uint32_t tab, uint32_t tabc, kpm_graph **out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,163 @@
+// libkpm C-ABI: context, memory and error plumbing (include/kpm.h).
+#include "kpm_internal.cuh"
+
+namespace kpm {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int stage_in(cudaStream_t s, const void *p, size_t bytes, DevBuf &tmp,
+             const void **dev) {
+  if (bytes == 0 || p == nullptr) {
+    *dev = p;
+    return KPM_OK;
+  }
+  if (is_device_ptr(p)) {
+    *dev = p;
+    return KPM_OK;
+  }
+  KPM_CUDA(cudaMalloc(&tmp.ptr, bytes));
+  KPM_CUDA(cudaMemcpyAsync(tmp.ptr, p, bytes, cudaMemcpyHostToDevice, s));
+  *dev = tmp.ptr;
+  return KPM_OK;
+}
+
+}  // namespace kpm
+
+using namespace kpm;
+
+extern "C" {
+
+int kpm_abi_version(void) { return KPM_ABI_VERSION; }
+
+const char *kpm_last_error(void) { return g_err; }
+
+int kpm_device_count(int *count) {
+  KPM_CHECK_ARG(count, "count is NULL");
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *count = c;
+  return KPM_OK;
+}
+
+int kpm_init(int device, kpm_ctx **out) {
+  KPM_CHECK_ARG(out, "out is NULL");
+  int count = 0;
+  kpm_device_count(&count);
+  if (count <= 0) {
+    set_error("no CUDA device visible");
+    return KPM_ENODEV;
+  }
+  KPM_CHECK_ARG(device >= 0 && device < count, "device %d out of range (%d)",
+                device, count);
+  KPM_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  KPM_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) {
+    set_error("device %d is sm_%d%d; libkpm is built for sm_100a only", device,
+              prop.major, prop.minor);
+    return KPM_ENODEV;
+  }
+  kpm_ctx *c = new kpm_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    set_error("cudaStreamCreate: %s", cudaGetErrorString(e));
+    return KPM_ECUDA;
+  }
+  *out = c;
+  return KPM_OK;
+}
+
+void kpm_finalize(kpm_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+void *kpm_ctx_stream(kpm_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+int kpm_ctx_synchronize(kpm_ctx *ctx) {
+  KPM_CHECK_ARG(ctx, "ctx is NULL");
+  KPM_CUDA(cudaStreamSynchronize(ctx->stream));
+  KPM_CUDA(cudaGetLastError());
+  return KPM_OK;
+}
+
+int kpm_device_alloc(kpm_ctx *ctx, int64_t bytes, void **out) {
+  KPM_CHECK_ARG(ctx && out && bytes >= 0, "bad arguments");
+  *out = nullptr;
+  if (bytes == 0) return KPM_OK;
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  KPM_CUDA(cudaMalloc(out, (size_t)bytes));
+  return KPM_OK;
+}
+
+int kpm_device_free(kpm_ctx *ctx, void *ptr) {
+  KPM_CHECK_ARG(ctx, "ctx is NULL");
+  if (ptr) {
+    KPM_CUDA(cudaStreamSynchronize(ctx->stream));
+    KPM_CUDA(cudaFree(ptr));
+  }
+  return KPM_OK;
+}
+
+int kpm_memcpy(kpm_ctx *ctx, void *dst, const void *src, int64_t bytes,
+               int kind) {
+  KPM_CHECK_ARG(ctx && bytes >= 0 && kind >= 0 && kind <= 2, "bad arguments");
+  if (bytes == 0) return KPM_OK;
+  cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
+                     : kind == 1 ? cudaMemcpyDeviceToHost
+                                 : cudaMemcpyDeviceToDevice;
+  KPM_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, k, ctx->stream));
+  return KPM_OK;
+}
+
+int kpm_host_alloc(int64_t bytes, void **out) {
+  KPM_CHECK_ARG(out && bytes >= 0, "bad arguments");
+  *out = nullptr;
+  if (bytes == 0) return KPM_OK;
+  KPM_CUDA(cudaMallocHost(out, (size_t)bytes));
+  return KPM_OK;
+}
+
+int kpm_mem_info(kpm_ctx *ctx, int64_t *free_bytes, int64_t *total_bytes) {
+  KPM_CHECK_ARG(ctx, "ctx is NULL");
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  size_t f = 0, t = 0;
+  KPM_CUDA(cudaMemGetInfo(&f, &t));
+  if (free_bytes) *free_bytes = (int64_t)f;
+  if (total_bytes) *total_bytes = (int64_t)t;
+  return KPM_OK;
+}
+
+int kpm_host_free(void *ptr) {
+  if (ptr) KPM_CUDA(cudaFreeHost(ptr));
+  return KPM_OK;
+}
+
+}  // extern "C"

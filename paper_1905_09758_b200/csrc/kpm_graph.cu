@@ -1,0 +1,478 @@
+// Device graph loader: edges -> symmetric CSR with
+// int64 row_ptr, int32 col_idx (sorted per row) and fp64 d^-1/2, plus the
+// load-balanced row-chunk schedule used by the recurrence kernels.
+//
+// Reference semantics (paths relative to /root/reference/pkg/src/netdos/):
+//   graph.py:69-81  _csr_from_canonical: both directions of each canonical
+//                   pair (a loop once), lexsort by (row, col), row_ptr by
+//                   counting + cumsum;
+//   graph.py:130-160 build_csr: canonicalise + merge duplicates;
+//   graph.py:47-54  degrees (unit weights, loop counted once);
+//   operators.py:108-110 dinv = deg > 0 ? 1/sqrt(deg) : 0 (IEEE sqrt, div).
+//
+// B200 design: one 64-bit key per stored entry, key = row << s | col with
+// 2^s > n, radix-sorted on exactly 2s bits (CUB onesweep over HBM), unique'd
+// in place, then row_ptr from the row boundaries of the sorted keys -- no
+// atomics, so the CSR is deterministic and bit-identical to the reference.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "kpm_internal.cuh"
+
+namespace kpm {
+
+static constexpr uint64_t kSentinel = ~0ull;
+
+static int key_bits(int64_t n) {
+  int s = 1;
+  while ((int64_t(1) << s) <= n) ++s;  // 2^s > n: row 2^s-1 never occurs
+  return s;
+}
+
+__global__ void edges_to_keys(const int64_t *__restrict__ u,
+                              const int64_t *__restrict__ v, int64_t m,
+                              int64_t n, int s, int keep_loops,
+                              uint64_t *__restrict__ keys, int *bad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = u[e], b = v[e];
+    uint64_t k0 = kSentinel, k1 = kSentinel;
+    if (a < 0 || b < 0 || a >= n || b >= n) {
+      atomicOr(bad, 1);
+    } else if (a == b) {
+      if (keep_loops) k0 = ((uint64_t)a << s) | (uint64_t)a;
+    } else {
+      k0 = ((uint64_t)a << s) | (uint64_t)b;
+      k1 = ((uint64_t)b << s) | (uint64_t)a;
+    }
+    keys[2 * e] = k0;
+    keys[2 * e + 1] = k1;
+  }
+}
+
+// Philox4x32-10 (Salmon et al., SC'11): the R-MAT harness generator.
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0,
+                                              uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+__device__ __forceinline__ void rmat_draw(uint64_t e, int scale, uint32_t k0,
+                                          uint32_t k1, uint32_t ta,
+                                          uint32_t tab, uint32_t tabc,
+                                          int64_t &a, int64_t &b) {
+  uint32_t w[4];
+  a = 0;
+  b = 0;
+  for (int l = 0; l < scale; ++l) {
+    if ((l & 3) == 0) {
+      w[0] = (uint32_t)e;
+      w[1] = (uint32_t)(e >> 32);
+      w[2] = (uint32_t)(l >> 2);
+      w[3] = 0u;
+      philox4x32_10(w, k0, k1);
+    }
+    uint32_t r = w[l & 3];
+    int bu = r >= tab;
+    int bv = (r >= ta && r < tab) || r >= tabc;
+    a = (a << 1) | bu;
+    b = (b << 1) | bv;
+  }
+}
+
+__global__ void rmat_edges_kernel(int scale, uint64_t seed, uint32_t ta,
+                                  uint32_t tab, uint32_t tabc, int64_t e0,
+                                  int64_t count, int64_t *u, int64_t *v) {
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a, b;
+    rmat_draw((uint64_t)(e0 + t), scale, k0, k1, ta, tab, tabc, a, b);
+    u[t] = a;
+    v[t] = b;
+  }
+}
+
+__global__ void rmat_keys_kernel(int scale, uint64_t seed, uint32_t ta,
+                                 uint32_t tab, uint32_t tabc, int64_t m,
+                                 int s, uint64_t *__restrict__ keys) {
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a, b;
+    rmat_draw((uint64_t)e, scale, k0, k1, ta, tab, tabc, a, b);
+    uint64_t k0v = kSentinel, k1v = kSentinel;
+    if (a != b) {
+      k0v = ((uint64_t)a << s) | (uint64_t)b;
+      k1v = ((uint64_t)b << s) | (uint64_t)a;
+    }
+    keys[2 * e] = k0v;
+    keys[2 * e + 1] = k1v;
+  }
+}
+
+// row_ptr[r] = index of the first key with row >= r (keys sorted, unique).
+__global__ void keys_to_csr(const uint64_t *__restrict__ keys, int64_t nnz,
+                            int s, int64_t *__restrict__ row_ptr,
+                            int32_t *__restrict__ col) {
+  const uint64_t mask = (uint64_t(1) << s) - 1;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t key = keys[k];
+    int64_t r = (int64_t)(key >> s);
+    int64_t rp = k > 0 ? (int64_t)(keys[k - 1] >> s) : -1;
+    for (int64_t q = rp + 1; q <= r; ++q) row_ptr[q] = k;
+    col[k] = (int32_t)(key & mask);
+  }
+}
+
+__global__ void fill_tail_rows(int64_t *row_ptr, int64_t from, int64_t n,
+                               int64_t nnz) {
+  for (int64_t q = from + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+       q <= n; q += (int64_t)gridDim.x * blockDim.x)
+    row_ptr[q] = nnz;
+}
+
+// graph.py:47-54 + operators.py:108-109 with IEEE-exact sqrt and division.
+__global__ void dinv_kernel(const int64_t *__restrict__ row_ptr, int64_t n,
+                            double *__restrict__ dinv,
+                            unsigned long long *max_deg) {
+  unsigned long long local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t d = row_ptr[i + 1] - row_ptr[i];
+    dinv[i] = d > 0 ? __ddiv_rn(1.0, __dsqrt_rn((double)d)) : 0.0;
+    if ((unsigned long long)d > local) local = (unsigned long long)d;
+  }
+  for (int o = 16; o > 0; o >>= 1)
+    local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(max_deg, local);
+}
+
+// Chunk c covers rows [start[c], start[c+1]); boundaries split the prefix
+// cost row_ptr[i] + kRowCost*i evenly.  Depends on the graph only.
+static constexpr int64_t kRowCost = 8;
+
+__global__ void chunk_bounds(const int64_t *__restrict__ row_ptr, int64_t n,
+                             int32_t n_chunks, int64_t target,
+                             int32_t *__restrict__ start) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > n_chunks) return;
+  if (c == 0) { start[0] = 0; return; }
+  if (c == n_chunks) { start[c] = (int32_t)n; return; }
+  int64_t want = (int64_t)c * target;
+  int64_t lo = 0, hi = n;  // first i with cost(i) >= want
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (row_ptr[mid] + kRowCost * mid >= want) hi = mid; else lo = mid + 1;
+  }
+  start[c] = (int32_t)lo;
+}
+
+static int grid_for(int64_t work, int threads = 256) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 64) b = 148 * 64;
+  return (int)b;
+}
+
+int finish_graph(kpm_graph *g) {
+  cudaStream_t st = g->ctx->stream;
+  unsigned long long *dmax = nullptr;
+  KPM_CUDA(cudaMallocAsync(&dmax, sizeof(unsigned long long), st));
+  KPM_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
+  if (g->n > 0)
+    dinv_kernel<<<grid_for(g->n), 256, 0, st>>>(g->row_ptr, g->n, g->dinv, dmax);
+  unsigned long long hmax = 0;
+  KPM_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof(hmax), cudaMemcpyDeviceToHost, st));
+  KPM_CUDA(cudaFreeAsync(dmax, st));
+  // schedule: a fixed denominator (148 SMs x 32) keeps chunks independent of
+  // the device and of the probe count, so reductions are reproducible.
+  int64_t total = g->nnz + kRowCost * g->n;
+  int64_t target = (total + 148 * 32 - 1) / (148 * 32);
+  if (target < 256) target = 256;
+  int64_t nch = (total + target - 1) / target;
+  if (nch < 1) nch = 1;
+  g->n_chunks = (int32_t)nch;
+  KPM_CUDA(cudaMalloc(&g->chunk_start, sizeof(int32_t) * (nch + 1)));
+  chunk_bounds<<<(int)((nch + 1 + 255) / 256), 256, 0, st>>>(
+      g->row_ptr, g->n, g->n_chunks, target, g->chunk_start);
+  KPM_CUDA(cudaGetLastError());
+  KPM_CUDA(cudaStreamSynchronize(st));
+  g->max_degree = (int64_t)hmax;
+  return KPM_OK;
+}
+
+// keys: 2m entries (sentinels allowed); consumes and frees keys/alt.
+static int keys_to_graph(kpm_ctx *ctx, int64_t n, int s, uint64_t *keys,
+                         uint64_t *alt, int64_t nkeys, kpm_graph **out) {
+  cudaStream_t st = ctx->stream;
+  int64_t nnz = 0;
+  if (nkeys > 0) {
+    cub::DoubleBuffer<uint64_t> db(keys, alt);
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, db, nkeys, 0, 2 * s, st);
+    void *tmp = nullptr;
+    KPM_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, db, nkeys, 0, 2 * s, st);
+    KPM_CUDA(cudaGetLastError());
+    KPM_CUDA(cudaFreeAsync(tmp, st));
+    uint64_t *sorted = db.Current(), *other = db.Alternate();
+    int64_t *d_nsel = nullptr;
+    KPM_CUDA(cudaMallocAsync(&d_nsel, sizeof(int64_t), st));
+    tmp_bytes = 0;
+    cub::DeviceSelect::Unique(nullptr, tmp_bytes, sorted, other, d_nsel, nkeys, st);
+    KPM_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    cub::DeviceSelect::Unique(tmp, tmp_bytes, sorted, other, d_nsel, nkeys, st);
+    KPM_CUDA(cudaGetLastError());
+    KPM_CUDA(cudaFreeAsync(tmp, st));
+    int64_t nsel = 0;
+    KPM_CUDA(cudaMemcpyAsync(&nsel, d_nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    KPM_CUDA(cudaFreeAsync(d_nsel, st));
+    uint64_t last = 0;
+    KPM_CUDA(cudaStreamSynchronize(st));
+    if (nsel > 0) {
+      KPM_CUDA(cudaMemcpy(&last, other + nsel - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    }
+    // the sentinel (all sorted bits set) sorts last and is not a real key
+    nnz = (nsel > 0 && last == kSentinel) ? nsel - 1 : nsel;
+    keys = other;  // unique keys live here now
+    alt = sorted;
+  }
+  KPM_CHECK_ARG(n < (int64_t(1) << 31), "n must be < 2^31 (int32 col_idx)");
+  kpm_graph *g = new kpm_graph();
+  g->ctx = ctx;
+  g->n = n;
+  g->nnz = nnz;
+  cudaError_t e1 = cudaMalloc(&g->row_ptr, sizeof(int64_t) * (n + 1));
+  cudaError_t e2 = cudaMalloc(&g->col_idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1));
+  cudaError_t e3 = cudaMalloc(&g->dinv, sizeof(double) * (n > 0 ? n : 1));
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+    kpm_graph_free(g);
+    set_error("graph allocation failed (n=%lld nnz=%lld)", (long long)n, (long long)nnz);
+    return KPM_ENOMEM;
+  }
+  if (nnz > 0) {
+    keys_to_csr<<<grid_for(nnz), 256, 0, st>>>(keys, nnz, s, g->row_ptr, g->col_idx);
+    uint64_t lastkey = 0;
+    KPM_CUDA(cudaMemcpyAsync(&lastkey, keys + nnz - 1, sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, st));
+    KPM_CUDA(cudaStreamSynchronize(st));
+    int64_t last_row = (int64_t)(lastkey >> s);
+    fill_tail_rows<<<grid_for(n - last_row), 256, 0, st>>>(g->row_ptr, last_row + 1, n, nnz);
+  } else {
+    fill_tail_rows<<<grid_for(n + 1), 256, 0, st>>>(g->row_ptr, 0, n, 0);
+  }
+  KPM_CUDA(cudaGetLastError());
+  KPM_CUDA(cudaStreamSynchronize(st));
+  if (keys) cudaFree(keys);
+  if (alt) cudaFree(alt);
+  int rc = finish_graph(g);
+  if (rc != KPM_OK) {
+    kpm_graph_free(g);
+    return rc;
+  }
+  *out = g;
+  return KPM_OK;
+}
+
+__global__ void idx64_to_32(const int64_t *__restrict__ in, int64_t m,
+                            int64_t n, int32_t *__restrict__ out, int *bad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x = in[e];
+    if (x < 0 || x >= n) atomicOr(bad, 1);
+    out[e] = (int32_t)x;
+  }
+}
+
+}  // namespace kpm
+
+using namespace kpm;
+
+extern "C" {
+
+int kpm_graph_from_edges(kpm_ctx *ctx, int64_t n, const int64_t *u,
+                         const int64_t *v, int64_t m, int keep_loops,
+                         kpm_graph **out) {
+  KPM_CHECK_ARG(ctx && out && n >= 0 && m >= 0, "bad arguments");
+  KPM_CHECK_ARG(m == 0 || (u && v), "u/v are NULL");
+  KPM_CHECK_ARG(n < (int64_t(1) << 31), "n must be < 2^31 (int32 col_idx)");
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  int s = key_bits(n);
+  uint64_t *keys = nullptr, *alt = nullptr;
+  if (m > 0) {
+    DevBuf tu, tv;
+    const void *du, *dv;
+    KPM_TRY(stage_in(st, u, sizeof(int64_t) * m, tu, &du));
+    KPM_TRY(stage_in(st, v, sizeof(int64_t) * m, tv, &dv));
+    KPM_CUDA(cudaMalloc(&keys, sizeof(uint64_t) * 2 * m));
+    KPM_CUDA(cudaMalloc(&alt, sizeof(uint64_t) * 2 * m));
+    int *bad = nullptr;
+    KPM_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+    KPM_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    edges_to_keys<<<grid_for(m), 256, 0, st>>>((const int64_t *)du, (const int64_t *)dv,
+                                               m, n, s, keep_loops, keys, bad);
+    int hbad = 0;
+    KPM_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    KPM_CUDA(cudaFreeAsync(bad, st));
+    KPM_CUDA(cudaStreamSynchronize(st));
+    if (hbad) {
+      cudaFree(keys);
+      cudaFree(alt);
+      set_error("node ids must be in [0, n)");
+      return KPM_EINVAL;
+    }
+  }
+  return keys_to_graph(ctx, n, s, keys, alt, 2 * m, out);
+}
+
+int kpm_graph_rmat(kpm_ctx *ctx, int scale, int64_t n_edges, uint64_t seed,
+                   uint32_t ta, uint32_t tab, uint32_t tabc, kpm_graph **out) {
+  KPM_CHECK_ARG(ctx && out && scale >= 1 && scale <= 30 && n_edges >= 0,
+                "bad arguments");
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  int64_t n = int64_t(1) << scale;
+  int s = key_bits(n);
+  uint64_t *keys = nullptr, *alt = nullptr;
+  if (n_edges > 0) {
+    KPM_CUDA(cudaMalloc(&keys, sizeof(uint64_t) * 2 * n_edges));
+    KPM_CUDA(cudaMalloc(&alt, sizeof(uint64_t) * 2 * n_edges));
+    rmat_keys_kernel<<<grid_for(n_edges), 256, 0, ctx->stream>>>(
+        scale, seed, ta, tab, tabc, n_edges, s, keys);
+    KPM_CUDA(cudaGetLastError());
+  }
+  return keys_to_graph(ctx, n, s, keys, alt, 2 * n_edges, out);
+}
+
+int kpm_rmat_edges(kpm_ctx *ctx, int scale, uint64_t seed, uint32_t ta,
+                   uint32_t tab, uint32_t tabc, int64_t e0, int64_t count,
+                   int64_t *u, int64_t *v) {
+  KPM_CHECK_ARG(ctx && u && v && scale >= 1 && scale <= 30 && e0 >= 0 && count >= 0,
+                "bad arguments");
+  KPM_CHECK_ARG(is_device_ptr(u) && is_device_ptr(v), "u/v must be device buffers");
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  if (count > 0)
+    rmat_edges_kernel<<<grid_for(count), 256, 0, ctx->stream>>>(scale, seed, ta, tab,
+                                                                tabc, e0, count, u, v);
+  KPM_CUDA(cudaGetLastError());
+  return KPM_OK;
+}
+
+int kpm_graph_from_csr(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
+                       const int64_t *indices, int64_t nnz,
+                       const double *values, double shift, double scale,
+                       kpm_graph **out) {
+  KPM_CHECK_ARG(ctx && out && n >= 0 && nnz >= 0 && indptr, "bad arguments");
+  KPM_CHECK_ARG(nnz == 0 || indices, "indices is NULL");
+  KPM_CHECK_ARG(n < (int64_t(1) << 31), "n must be < 2^31 (int32 col_idx)");
+  KPM_CHECK_ARG(values || (shift == 0.0 && scale == 1.0),
+                "implicit normalized adjacency takes shift 0, scale 1");
+  KPM_CHECK_ARG(scale != 0.0, "scale must be nonzero");
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  kpm_graph *g = new kpm_graph();
+  g->ctx = ctx;
+  g->n = n;
+  g->nnz = nnz;
+  g->shift = shift;
+  g->scale = scale;
+  auto fail = [&](int rc) { kpm_graph_free(g); return rc; };
+  if (cudaMalloc(&g->row_ptr, sizeof(int64_t) * (n + 1)) != cudaSuccess ||
+      cudaMalloc(&g->col_idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1)) != cudaSuccess ||
+      cudaMalloc(&g->dinv, sizeof(double) * (n > 0 ? n : 1)) != cudaSuccess ||
+      (values && cudaMalloc(&g->values, sizeof(double) * (nnz > 0 ? nnz : 1)) != cudaSuccess)) {
+    set_error("graph allocation failed");
+    return fail(KPM_ENOMEM);
+  }
+  cudaError_t e = cudaMemcpyAsync(g->row_ptr, indptr, sizeof(int64_t) * (n + 1),
+                                  cudaMemcpyDefault, st);
+  if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); return fail(KPM_ECUDA); }
+  int64_t ends[2] = {0, 0};
+  e = cudaMemcpyAsync(ends, g->row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(ends + 1, g->row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); return fail(KPM_ECUDA); }
+  if (ends[0] != 0 || ends[1] != nnz) {
+    set_error("indptr must start at 0 and end at nnz");
+    return fail(KPM_EINVAL);
+  }
+  if (nnz > 0) {
+    DevBuf ti;
+    const void *di;
+    int rc = stage_in(st, indices, sizeof(int64_t) * nnz, ti, &di);
+    if (rc != KPM_OK) return fail(rc);
+    int *bad = nullptr;
+    cudaMalloc(&bad, sizeof(int));
+    cudaMemsetAsync(bad, 0, sizeof(int), st);
+    idx64_to_32<<<grid_for(nnz), 256, 0, st>>>((const int64_t *)di, nnz, n, g->col_idx, bad);
+    int hbad = 0;
+    cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    e = cudaStreamSynchronize(st);
+    cudaFree(bad);
+    if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); return fail(KPM_ECUDA); }
+    if (hbad) { set_error("column index out of range"); return fail(KPM_EINVAL); }
+    if (values) {
+      e = cudaMemcpyAsync(g->values, values, sizeof(double) * nnz, cudaMemcpyDefault, st);
+      if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); return fail(KPM_ECUDA); }
+    }
+  }
+  int rc = finish_graph(g);
+  if (rc != KPM_OK) return fail(rc);
+  *out = g;
+  return KPM_OK;
+}
+
+int kpm_graph_info(kpm_graph *g, int64_t *n, int64_t *nnz, int64_t *max_degree) {
+  KPM_CHECK_ARG(g, "graph is NULL");
+  if (n) *n = g->n;
+  if (nnz) *nnz = g->nnz;
+  if (max_degree) *max_degree = g->max_degree;
+  return KPM_OK;
+}
+
+int kpm_graph_export(kpm_graph *g, int64_t *row_ptr, int32_t *col_idx,
+                     double *dinv) {
+  KPM_CHECK_ARG(g, "graph is NULL");
+  cudaStream_t st = g->ctx->stream;
+  KPM_CUDA(cudaSetDevice(g->ctx->device));
+  if (row_ptr)
+    KPM_CUDA(cudaMemcpyAsync(row_ptr, g->row_ptr, sizeof(int64_t) * (g->n + 1),
+                             cudaMemcpyDefault, st));
+  if (col_idx && g->nnz)
+    KPM_CUDA(cudaMemcpyAsync(col_idx, g->col_idx, sizeof(int32_t) * g->nnz,
+                             cudaMemcpyDefault, st));
+  if (dinv && g->n)
+    KPM_CUDA(cudaMemcpyAsync(dinv, g->dinv, sizeof(double) * g->n, cudaMemcpyDefault, st));
+  KPM_CUDA(cudaStreamSynchronize(st));
+  return KPM_OK;
+}
+
+void kpm_graph_free(kpm_graph *g) {
+  if (!g) return;
+  if (g->ctx) {
+    cudaSetDevice(g->ctx->device);
+    cudaStreamSynchronize(g->ctx->stream);
+  }
+  cudaFree(g->row_ptr);
+  cudaFree(g->col_idx);
+  cudaFree(g->dinv);
+  cudaFree(g->values);
+  cudaFree(g->chunk_start);
+  delete g;
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Internal types and helpers shared by the libkpm translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/kpm.h"
+
+namespace kpm {
+
+void set_error(const char *fmt, ...);
+
+#define KPM_CUDA(expr)                                                         \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      kpm::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,              \
+                     cudaGetErrorString(_e));                                  \
+      return _e == cudaErrorMemoryAllocation ? KPM_ENOMEM : KPM_ECUDA;         \
+    }                                                                          \
+  } while (0)
+
+#define KPM_CHECK_ARG(cond, ...)                                               \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      kpm::set_error(__VA_ARGS__);                                             \
+      return KPM_EINVAL;                                                       \
+    }                                                                          \
+  } while (0)
+
+#define KPM_TRY(expr)                                                          \
+  do {                                                                         \
+    int _s = (expr);                                                           \
+    if (_s != KPM_OK) return _s;                                               \
+  } while (0)
+
+// true when p is device (or managed) memory usable in kernels
+bool is_device_ptr(const void *p);
+
+// Stage a host-or-device input array on the device: returns a device pointer
+// (p itself when already on the device; otherwise a temporary owned by tmp).
+struct DevBuf {
+  void *ptr = nullptr;
+  ~DevBuf() { if (ptr) cudaFree(ptr); }
+  DevBuf() = default;
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+};
+int stage_in(cudaStream_t s, const void *p, size_t bytes, DevBuf &tmp,
+             const void **dev);
+
+}  // namespace kpm
+
+struct kpm_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+};
+
+// Device CSR: int64 row_ptr, int32 col_idx, fp64 dinv (implicit normalized
+// adjacency) or fp64 values + (shift, scale) (explicit operator).
+struct kpm_graph {
+  kpm_ctx *ctx = nullptr;
+  int64_t n = 0, nnz = 0, max_degree = 0;
+  int64_t *row_ptr = nullptr;   // n+1
+  int32_t *col_idx = nullptr;   // nnz
+  double *dinv = nullptr;       // n (always computed from row degree)
+  double *values = nullptr;     // nnz, explicit mode only
+  double shift = 0.0, scale = 1.0;
+  // load-balanced schedule (depends on the graph only, never on k)
+  int32_t n_chunks = 0;
+  int32_t *chunk_start = nullptr;  // n_chunks+1 row boundaries
+};
+
+struct kpm_run {
+  kpm_graph *g = nullptr;
+  int64_t k = 0;      // probes in this batch
+  int64_t ld = 0;     // padded row stride (doubles)
+  int cpl = 1;        // columns per lane (1, 2, 4)
+  int32_t mode = 0, m_max = 0, flags = 0;
+  int32_t total_steps = 0, done_steps = 0;
+  bool have_probes = false;
+  double *z = nullptr;        // probes (DIRECT/LDOS), n x ld
+  double *a = nullptr, *b = nullptr;  // recurrence blocks
+  double *cur = nullptr, *prev = nullptr;  // T_k (gather source), T_{k-1}
+  int32_t k_index = 0;        // index of the block in `cur`
+  double *partial = nullptr;  // n_chunks x 2 x ld
+  double *contrib = nullptr;  // (m_max+1) x ld (global modes)
+  double *ldos = nullptr;     // n x (m_max+1) (LDOS)
+  double *den = nullptr;      // n (LDOS)
+  int32_t *flag = nullptr;    // [0]: non-finite seen; [1..2]: zero-mass node
+};

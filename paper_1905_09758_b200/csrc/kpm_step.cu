@@ -1,0 +1,800 @@
+// The fused KPM recurrence step and the run API.
+//
+// One launch per recurrence step computes, for every row i and probe column c,
+//     acc      = sum_{jj in row i, stored order} h_ij * X[j, c]
+//     T_{k+1}  = 2*acc - T_{k-1}            (T_1 = acc)
+// with h_ij = dinv_i * dinv_j formed on the fly (H is never stored), every
+// multiply and add separately rounded (__dmul_rn/__dadd_rn, no FMA), i.e.
+// exactly the arithmetic of the reference's _spmv.pyx:11-22 _row followed by
+// kpm.py:86-87 (`t_next *= 2.0; t_next -= t_prev`).  The T blocks are
+// therefore BIT-IDENTICAL to the reference's _recurrence (kpm.py:73-89).
+// In the same pass the kernel reduces the moment contributions:
+//   DOUBLING  per probe <T_{k+1},T_k> and <T_{k+1},T_{k+1}>, giving
+//             mu_{2k+1} = 2<T_{k+1},T_k> - mu_1 and mu_{2k+2} = 2<T_{k+1},T_{k+1}> - mu_0
+//             (T_{2k} = 2 T_k^2 - I), ceil(M/2) steps for M moments;
+//   DIRECT    per probe z^T T_{k+1} (kpm.py:107-108 einsum 'ij,ij->j');
+//   LDOS      per node sum_c z_ic T_{k+1,ic} (kpm.py:135-136 'ij,ij->i'),
+//             written straight into the (n, M+1) result as num/den.
+// Global sums are deterministic: rows are grouped into load-balanced chunks
+// that depend only on the graph (kpm_graph.cu), each warp of a CTA owns a
+// fixed row subsequence, warps combine in fixed order into one partial per
+// chunk, and a finalize kernel sums chunks in fixed order.
+//
+// Layout: X/T blocks are n x ld fp64 row-major (the reference's C-contiguous
+// n x nz probe block, rows padded to ld = multiple of the lane vector width);
+// one warp owns one row, lane l owns columns [l*C, l*C+C) of each 32*C-wide
+// column tile, so every gathered neighbour row is one coalesced 8*ld-byte
+// read; neighbour ids / weights are loaded 32 at a time by the lanes and
+// broadcast with shuffles, and U gathers are kept in flight per warp.
+#include "kpm_internal.cuh"
+
+namespace kpm {
+
+enum { MODE_DBL = 0, MODE_DIRECT = 1, MODE_LDOS = 2 };
+
+struct StepParams {
+  const int64_t *row_ptr;
+  const int32_t *col;
+  const double *dinv;
+  const double *vals;      // explicit operator values (or nullptr)
+  double shift, scale;     // explicit epilogue
+  const double *X;         // T_k, gather source (read-only in this launch)
+  const double *Xprev;     // T_{k-1} own rows (may alias Y)
+  double *Y;               // T_{k+1}
+  const double *Z;         // probes (DIRECT / LDOS)
+  const double *den;       // LDOS normaliser
+  double *ldos;            // LDOS result, n x (M+1)
+  int ldos_col;            // moment index written this step
+  int ldos_stride;         // M+1
+  int ldos_raw;            // KPM_LDOS_RAW
+  int64_t ld;
+  const int32_t *chunk_start;
+  double *partial;         // n_chunks x 2 x ld
+  int32_t *flag;
+};
+
+template <int C>
+__device__ __forceinline__ void ld_vec(const double *p, double (&v)[C]) {
+  if constexpr (C == 1) {
+    v[0] = __ldg(p);
+  } else if constexpr (C == 2) {
+    double2 t = __ldg(reinterpret_cast<const double2 *>(p));
+    v[0] = t.x; v[1] = t.y;
+  } else {
+    double2 t0 = __ldg(reinterpret_cast<const double2 *>(p));
+    double2 t1 = __ldg(reinterpret_cast<const double2 *>(p + 2));
+    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
+  }
+}
+
+// plain (coherent) load: Xprev may alias Y
+template <int C>
+__device__ __forceinline__ void ld_vec_rw(const double *p, double (&v)[C]) {
+  if constexpr (C == 1) {
+    v[0] = *p;
+  } else if constexpr (C == 2) {
+    double2 t = *reinterpret_cast<const double2 *>(p);
+    v[0] = t.x; v[1] = t.y;
+  } else {
+    double2 t0 = *reinterpret_cast<const double2 *>(p);
+    double2 t1 = *reinterpret_cast<const double2 *>(p + 2);
+    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void st_vec(double *p, const double (&v)[C]) {
+  if constexpr (C == 1) {
+    *p = v[0];
+  } else if constexpr (C == 2) {
+    *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
+  } else {
+    *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
+    *reinterpret_cast<double2 *>(p + 2) = make_double2(v[2], v[3]);
+  }
+}
+
+__device__ __forceinline__ double warp_sum_fixed(double x) {
+  // fixed butterfly: same tree for every call -> deterministic
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+// INIT: step-0 reductions (mu_0 = z.z per probe; LDOS den and column 0).
+template <int C, int MODE, bool EXPL, bool FIRST, bool INIT, int U>
+__global__ void __launch_bounds__(256)
+kpm_step_kernel(const StepParams p) {
+  extern __shared__ double sacc[];  // [W][2][ld] (global modes)
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int W = blockDim.x >> 5;
+  const int64_t ld = p.ld;
+  const int ntiles = (int)((ld + 32 * C - 1) / (32 * C));
+  double *my = sacc + (size_t)warp * 2 * ld;
+  if constexpr (MODE != MODE_LDOS) {
+    for (int64_t e = lane; e < 2 * ld; e += 32) my[e] = 0.0;
+    __syncwarp();
+  }
+  const int chunk = blockIdx.x;
+  const int r0 = p.chunk_start[chunk], r1 = p.chunk_start[chunk + 1];
+
+  for (int i = r0 + warp; i < r1; i += W) {
+    const size_t rowoff = (size_t)i * ld;
+    int64_t beg = 0, end = 0;
+    double di = 0.0;
+    if constexpr (!INIT) {
+      beg = p.row_ptr[i];
+      end = p.row_ptr[i + 1];
+      if constexpr (!EXPL) di = p.dinv[i];
+    }
+    double lsum = 0.0;  // LDOS lane partial
+    for (int t = 0; t < ntiles; ++t) {
+      const int64_t c0 = ((int64_t)t * 32 + lane) * C;
+      const bool active = c0 < ld;
+      double acc[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = 0.0;
+      if constexpr (!INIT) {
+        for (int64_t base = beg; base < end; base += 32) {
+          const int cnt = (int)min((int64_t)32, end - base);
+          int jl = 0;
+          double hl = 0.0;
+          if (lane < cnt) {
+            jl = p.col[base + lane];
+            if constexpr (EXPL) hl = p.vals[base + lane];
+            else hl = __dmul_rn(di, __ldg(p.dinv + jl));
+          }
+          for (int q = 0; q < cnt; q += U) {
+            double v[U][C];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int j = __shfl_sync(0xffffffffu, jl, (q + u) & 31);
+#pragma unroll
+              for (int c = 0; c < C; ++c) v[u][c] = 0.0;
+              if (q + u < cnt && active) ld_vec<C>(p.X + (size_t)j * ld + c0, v[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const double h = __shfl_sync(0xffffffffu, hl, (q + u) & 31);
+              if (q + u < cnt) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[u][c]));
+              }
+            }
+          }
+        }
+      }
+      if (!active) continue;
+      double y[C], xo[C], pv[C], zv[C];
+      if constexpr (INIT) {
+        ld_vec<C>(p.X + rowoff + c0, y);  // T_0 = z
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) y[c] = acc[c];
+        if constexpr (EXPL || MODE == MODE_DBL) ld_vec<C>(p.X + rowoff + c0, xo);
+        if constexpr (EXPL) {
+          // operators.py:144-147: y -= shift*x; y /= scale (separate roundings)
+          if (p.shift != 0.0) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) y[c] = __dsub_rn(y[c], __dmul_rn(p.shift, xo[c]));
+          }
+          if (p.scale != 1.0) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) y[c] = __ddiv_rn(y[c], p.scale);
+          }
+        }
+        if constexpr (!FIRST) {
+          ld_vec_rw<C>(p.Xprev + rowoff + c0, pv);
+#pragma unroll
+          for (int c = 0; c < C; ++c) y[c] = __dsub_rn(__dmul_rn(2.0, y[c]), pv[c]);
+        }
+        st_vec<C>(p.Y + rowoff + c0, y);
+      }
+      if constexpr (MODE == MODE_DIRECT || MODE == MODE_LDOS) {
+        if constexpr (INIT) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) zv[c] = y[c];
+        } else {
+          ld_vec<C>(p.Z + rowoff + c0, zv);
+        }
+      }
+      if constexpr (MODE == MODE_DBL) {
+        double *s1 = my + c0, *s2 = my + ld + c0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          if constexpr (INIT) {
+            s1[c] = __dadd_rn(s1[c], __dmul_rn(y[c], y[c]));
+          } else {
+            s1[c] = __dadd_rn(s1[c], __dmul_rn(y[c], xo[c]));
+            s2[c] = __dadd_rn(s2[c], __dmul_rn(y[c], y[c]));
+          }
+        }
+      } else if constexpr (MODE == MODE_DIRECT) {
+        double *s1 = my + c0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) s1[c] = __dadd_rn(s1[c], __dmul_rn(zv[c], y[c]));
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) lsum = __dadd_rn(lsum, __dmul_rn(zv[c], y[c]));
+      }
+    }
+    if constexpr (MODE == MODE_LDOS) {
+      const double num = warp_sum_fixed(lsum);
+      if (lane == 0) {
+        const size_t o = (size_t)i * p.ldos_stride + p.ldos_col;
+        if (!isfinite(num)) atomicOr(p.flag, 1);
+        if constexpr (INIT) {
+          // kpm.py:144-147: den = einsum(z, z) (same reduction as num[0])
+          double *den = const_cast<double *>(p.den);
+          den[i] = num;
+          if (!p.ldos_raw && num == 0.0) atomicMin(p.flag + 1, i);
+        }
+        p.ldos[o] = num;  // raw num[m, i]; kpm_run_result applies /den
+      }
+    }
+  }
+  if constexpr (MODE != MODE_LDOS) {
+    __syncthreads();
+    // combine warps in fixed order -> one partial per chunk
+    const int nred = (MODE == MODE_DBL && !INIT) ? 2 : 1;
+    double *out = p.partial + (size_t)chunk * 2 * ld;
+    for (int64_t e = threadIdx.x; e < nred * ld; e += blockDim.x) {
+      double s = sacc[e];
+      for (int w = 1; w < W; ++w) s = __dadd_rn(s, sacc[(size_t)w * 2 * ld + e]);
+      out[e] = s;
+    }
+  }
+}
+
+// Sum chunk partials in fixed order and write contrib rows.
+//   which = 0: INIT       contrib[0] = S1
+//   which = 1: DIRECT     contrib[m] = S1
+//   which = 2: DBL step s contrib[2s-1] = 2 S1 - mu_1 (s==1: S1),
+//                         contrib[2s]   = 2 S2 - mu_0     (if 2s <= M)
+__global__ void finalize_kernel(const double *__restrict__ partial,
+                                int n_chunks, int64_t ld, int64_t k,
+                                int which, int m, int m_max,
+                                double *__restrict__ contrib) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int nred = which == 2 ? 2 : 1;
+  if (gw >= nred * k) return;
+  const int red = (int)(gw / k);
+  const int64_t c = gw % k;
+  double s = 0.0;
+  for (int ch = lane; ch < n_chunks; ch += 32)
+    s = __dadd_rn(s, partial[(size_t)ch * 2 * ld + red * ld + c]);
+  s = warp_sum_fixed(s);
+  if (lane != 0) return;
+  if (which == 0) {
+    contrib[c] = s;
+  } else if (which == 1) {
+    contrib[(size_t)m * ld + c] = s;
+  } else {
+    // m = step index s >= 1 producing T_s
+    if (red == 0) {
+      const int row = 2 * m - 1;
+      if (row <= m_max)
+        contrib[(size_t)row * ld + c] = (m == 1) ? s : __dsub_rn(__dmul_rn(2.0, s), contrib[ld + c]);
+    } else {
+      const int row = 2 * m;
+      if (row <= m_max)
+        contrib[(size_t)row * ld + c] = __dsub_rn(__dmul_rn(2.0, s), contrib[c]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- dispatch
+template <int C, int MODE, bool INIT>
+static cudaError_t launch_c(const kpm_graph *g, const StepParams &p, bool expl,
+                            bool first, cudaStream_t st) {
+  constexpr int U = (C == 4) ? 4 : 8;
+  const int threads = 256;
+  size_t smem = (MODE == MODE_LDOS) ? 0 : (size_t)(threads / 32) * 2 * p.ld * sizeof(double);
+  void (*kern)(StepParams);
+  if (INIT) kern = kpm_step_kernel<C, MODE, false, true, true, U>;
+  else if (expl && first) kern = kpm_step_kernel<C, MODE, true, true, false, U>;
+  else if (expl) kern = kpm_step_kernel<C, MODE, true, false, false, U>;
+  else if (first) kern = kpm_step_kernel<C, MODE, false, true, false, U>;
+  else kern = kpm_step_kernel<C, MODE, false, false, false, U>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<g->n_chunks, threads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int MODE, bool INIT>
+static cudaError_t launch_mode(const kpm_graph *g, int cpl, const StepParams &p,
+                               bool expl, bool first, cudaStream_t st) {
+  switch (cpl) {
+    case 1: return launch_c<1, MODE, INIT>(g, p, expl, first, st);
+    case 2: return launch_c<2, MODE, INIT>(g, p, expl, first, st);
+    default: return launch_c<4, MODE, INIT>(g, p, expl, first, st);
+  }
+}
+
+static cudaError_t launch_step(const kpm_run *r, const StepParams &p, bool init,
+                               bool first, cudaStream_t st) {
+  const bool expl = r->g->values != nullptr;
+  if (r->g->n_chunks == 0) return cudaSuccess;
+  switch (r->mode) {
+    case KPM_MODE_DOS_DOUBLING:
+      return init ? launch_mode<MODE_DBL, true>(r->g, r->cpl, p, expl, first, st)
+                  : launch_mode<MODE_DBL, false>(r->g, r->cpl, p, expl, first, st);
+    case KPM_MODE_DOS_DIRECT:
+      return init ? launch_mode<MODE_DIRECT, true>(r->g, r->cpl, p, expl, first, st)
+                  : launch_mode<MODE_DIRECT, false>(r->g, r->cpl, p, expl, first, st);
+    default:
+      return init ? launch_mode<MODE_LDOS, true>(r->g, r->cpl, p, expl, first, st)
+                  : launch_mode<MODE_LDOS, false>(r->g, r->cpl, p, expl, first, st);
+  }
+}
+
+static StepParams base_params(const kpm_run *r) {
+  StepParams p{};
+  const kpm_graph *g = r->g;
+  p.row_ptr = g->row_ptr;
+  p.col = g->col_idx;
+  p.dinv = g->dinv;
+  p.vals = g->values;
+  p.shift = g->shift;
+  p.scale = g->scale;
+  p.Z = r->z;
+  p.den = r->den;
+  p.ldos = r->ldos;
+  p.ldos_stride = r->m_max + 1;
+  p.ldos_raw = (r->flags & KPM_LDOS_RAW) != 0;
+  p.ld = r->ld;
+  p.chunk_start = g->chunk_start;
+  p.partial = r->partial;
+  p.flag = r->flag;
+  return p;
+}
+
+static cudaError_t launch_finalize(const kpm_run *r, int which, int m, cudaStream_t st) {
+  const int nred = which == 2 ? 2 : 1;
+  const int64_t warps = nred * r->k;
+  const int threads = 256;
+  const int64_t blocks = (warps * 32 + threads - 1) / threads;
+  if (r->g->n_chunks == 0) return cudaSuccess;
+  finalize_kernel<<<(unsigned)blocks, threads, 0, st>>>(r->partial, r->g->n_chunks, r->ld,
+                                                       r->k, which, m, r->m_max, r->contrib);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------- probes (K0)
+// numpy Philox4x64-10 (Random123 constants) for make_probes(RADEMACHER).
+__device__ __forceinline__ void philox4x64_10(uint64_t c[4], uint64_t k0, uint64_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+    uint64_t hi0 = __umul64hi(M0, c[0]), lo0 = M0 * c[0];
+    uint64_t hi1 = __umul64hi(M1, c[2]), lo1 = M1 * c[2];
+    uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B97F4A7C15ull;
+    k1 += 0xBB67AE8584CAA73Bull;
+  }
+}
+
+// Element i of a column is bit 31 of the i-th 32-bit half-word of the
+// column's Philox stream (numpy: integers(0, 2) -> Lemire on next_uint32,
+// low half first; counter incremented before each 4-word block).
+__global__ void rademacher_kernel(int64_t n, int64_t ncols, const uint64_t *__restrict__ keys,
+                                  double *__restrict__ z, int64_t ldz, int64_t col0) {
+  const int64_t nblk = (n + 7) / 8;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nblk * ncols;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / ncols, j = t % ncols;
+    uint64_t c[4] = {(uint64_t)b + 1, 0, 0, 0};
+    philox4x64_10(c, keys[2 * j], keys[2 * j + 1]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t i = b * 8 + q;
+      if (i < n) {
+        const uint32_t half = (q & 1) ? (uint32_t)(c[q >> 1] >> 32) : (uint32_t)c[q >> 1];
+        z[i * ldz + col0 + j] = (half >> 31) ? -1.0 : 1.0;
+      }
+    }
+  }
+}
+
+// kpm.py:148-150: values = (num / den).T, or num * trace_scale (raw); the
+// num array is already node-major (n, M+1).
+__global__ void ldos_finish(double *__restrict__ v, const double *__restrict__ den,
+                            int64_t n, int64_t stride, int raw, double ts) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * stride;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const double x = v[t];
+    v[t] = raw ? __dmul_rn(x, ts) : __ddiv_rn(x, den[t / stride]);
+  }
+}
+
+__global__ void zero_pad_cols(double *z, int64_t n, int64_t k, int64_t ld) {
+  const int64_t w = ld - k;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * w;
+       t += (int64_t)gridDim.x * blockDim.x)
+    z[(t / w) * ld + k + t % w] = 0.0;
+}
+
+static int grid_of(int64_t work) {
+  int64_t b = (work + 255) / 256;
+  return (int)(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
+}
+
+// ------------------------------------------- standalone SpMM (L0 drop-in)
+// _spmv.pyx:11-22: out[i,c] = 0; out[i,c] += data[jj]*x[j,c] in stored order.
+__global__ void csr_matvec_kernel(int64_t n_rows, const int64_t *__restrict__ indptr,
+                                  const int64_t *__restrict__ indices,
+                                  const double *__restrict__ data,
+                                  const double *__restrict__ x, int64_t k,
+                                  double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n_rows; i += nw) {
+    const int64_t beg = indptr[i], end = indptr[i + 1];
+    for (int64_t c0 = 0; c0 < k; c0 += 32) {
+      const int64_t c = c0 + lane;
+      double acc = 0.0;
+      for (int64_t base = beg; base < end; base += 32) {
+        const int cnt = (int)min((int64_t)32, end - base);
+        int64_t jl = 0;
+        double wl = 0.0;
+        if (lane < cnt) {
+          jl = indices[base + lane];
+          wl = data[base + lane];
+        }
+        for (int q = 0; q < cnt; ++q) {
+          const int64_t j = __shfl_sync(0xffffffffu, jl, q);
+          const double w = __shfl_sync(0xffffffffu, wl, q);
+          if (c < k) acc = __dadd_rn(acc, __dmul_rn(w, x[j * k + c]));
+        }
+      }
+      if (c < k) out[i * k + c] = acc;
+    }
+  }
+}
+
+// ------------------------------------------ motif projection (K7)
+// motifs.py:400-403 per vector, groups of disjoint support in parallel.
+__global__ void filter_kernel(double *__restrict__ z, int64_t k, int64_t ldz,
+                              int64_t n_groups, const int64_t *__restrict__ gptr,
+                              const int64_t *__restrict__ vptr,
+                              const int64_t *__restrict__ vidx,
+                              const double *__restrict__ vval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < n_groups;
+       g += nw) {
+    for (int64_t vec = gptr[g]; vec < gptr[g + 1]; ++vec) {
+      const int64_t s0 = vptr[vec], s1 = vptr[vec + 1];
+      for (int64_t c = lane; c < k; c += 32) {
+        // coeff = val @ cols[idx] (sequential over the support)
+        double coeff = 0.0;
+        for (int64_t t = s0; t < s1; ++t)
+          coeff = __dadd_rn(coeff, __dmul_rn(vval[t], z[vidx[t] * ldz + c]));
+        // cols[idx] -= outer(val, coeff)
+        for (int64_t t = s0; t < s1; ++t) {
+          double *zz = z + vidx[t] * ldz + c;
+          *zz = __dsub_rn(*zz, __dmul_rn(vval[t], coeff));
+        }
+      }
+    }
+  }
+}
+
+}  // namespace kpm
+
+using namespace kpm;
+
+extern "C" {
+
+int kpm_run_create(kpm_graph *g, int64_t k, int32_t mode, int32_t m_max,
+                   int32_t flags, kpm_run **out) {
+  KPM_CHECK_ARG(g && out, "bad arguments");
+  KPM_CHECK_ARG(k >= 1, "need at least one probe column");
+  KPM_CHECK_ARG(m_max >= 0, "m_max must be >= 0");
+  KPM_CHECK_ARG(mode >= 0 && mode <= 2, "unknown mode %d", mode);
+  KPM_CHECK_ARG(k <= 1024 || mode == KPM_MODE_LDOS,
+                "at most 1024 probe columns per batch (got %lld)", (long long)k);
+  KPM_CUDA(cudaSetDevice(g->ctx->device));
+  kpm_run *r = new kpm_run();
+  r->g = g;
+  r->k = k;
+  r->cpl = k <= 32 ? 1 : (k <= 64 ? 2 : 4);
+  r->ld = (k + r->cpl - 1) / r->cpl * r->cpl;
+  r->mode = mode;
+  r->m_max = m_max;
+  r->flags = flags;
+  r->total_steps = mode == KPM_MODE_DOS_DOUBLING ? (m_max + 1) / 2 : m_max;
+  const size_t blk = sizeof(double) * (size_t)(g->n > 0 ? g->n : 1) * r->ld;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](void **p, size_t b) { if (e == cudaSuccess) e = cudaMalloc(p, b); };
+  A((void **)&r->a, blk);
+  if (m_max >= 1) A((void **)&r->b, blk);
+  if (mode != KPM_MODE_DOS_DOUBLING) A((void **)&r->z, blk);
+  A((void **)&r->flag, sizeof(int32_t) * 4);
+  if (mode == KPM_MODE_LDOS) {
+    A((void **)&r->ldos, sizeof(double) * (size_t)(g->n > 0 ? g->n : 1) * (m_max + 1));
+    A((void **)&r->den, sizeof(double) * (size_t)(g->n > 0 ? g->n : 1));
+  } else {
+    A((void **)&r->partial, sizeof(double) * (size_t)(g->n_chunks > 0 ? g->n_chunks : 1) * 2 * r->ld);
+    A((void **)&r->contrib, sizeof(double) * (size_t)(m_max + 1) * r->ld);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    kpm_run_free(r);
+    set_error("run allocation failed: %s", cudaGetErrorString(e));
+    return KPM_ENOMEM;
+  }
+  *out = r;
+  return KPM_OK;
+}
+
+static int run_after_probes(kpm_run *r) {
+  cudaStream_t st = r->g->ctx->stream;
+  const kpm_graph *g = r->g;
+  if (r->ld > r->k && g->n > 0)
+    zero_pad_cols<<<grid_of(g->n * (r->ld - r->k)), 256, 0, st>>>(r->a, g->n, r->k, r->ld);
+  if (r->z && g->n > 0)
+    KPM_CUDA(cudaMemcpyAsync(r->z, r->a, sizeof(double) * g->n * r->ld,
+                             cudaMemcpyDeviceToDevice, st));
+  int32_t init_flag[4] = {0, 0x7fffffff, 0, 0};
+  KPM_CUDA(cudaMemcpyAsync(r->flag, init_flag, sizeof(init_flag), cudaMemcpyHostToDevice, st));
+  if (r->contrib)
+    KPM_CUDA(cudaMemsetAsync(r->contrib, 0, sizeof(double) * (r->m_max + 1) * r->ld, st));
+  StepParams p = base_params(r);
+  p.X = r->a;
+  p.ldos_col = 0;
+  KPM_CUDA(launch_step(r, p, true, true, st));
+  if (r->mode != KPM_MODE_LDOS) KPM_CUDA(launch_finalize(r, 0, 0, st));
+  KPM_CUDA(cudaStreamSynchronize(st));  // init_flag lives on this stack
+  r->cur = r->a;
+  r->prev = nullptr;
+  r->k_index = 0;
+  r->done_steps = 0;
+  r->have_probes = true;
+  return KPM_OK;
+}
+
+int kpm_run_set_probes(kpm_run *r, const double *z, int64_t ldz) {
+  KPM_CHECK_ARG(r && (z || r->g->n == 0), "bad arguments");
+  KPM_CHECK_ARG(ldz >= r->k, "ldz < k");
+  KPM_CUDA(cudaSetDevice(r->g->ctx->device));
+  cudaStream_t st = r->g->ctx->stream;
+  if (r->g->n > 0)
+    KPM_CUDA(cudaMemcpy2DAsync(r->a, sizeof(double) * r->ld, z, sizeof(double) * ldz,
+                               sizeof(double) * r->k, r->g->n, cudaMemcpyDefault, st));
+  return run_after_probes(r);
+}
+
+int kpm_run_set_rademacher(kpm_run *r, const uint64_t *keys) {
+  KPM_CHECK_ARG(r && keys, "bad arguments");
+  KPM_CUDA(cudaSetDevice(r->g->ctx->device));
+  cudaStream_t st = r->g->ctx->stream;
+  DevBuf tk;
+  const void *dk;
+  KPM_TRY(stage_in(st, keys, sizeof(uint64_t) * 2 * r->k, tk, &dk));
+  const int64_t n = r->g->n;
+  if (n > 0)
+    rademacher_kernel<<<grid_of(((n + 7) / 8) * r->k), 256, 0, st>>>(
+        n, r->k, (const uint64_t *)dk, r->a, r->ld, 0);
+  KPM_CUDA(cudaGetLastError());
+  int rc = run_after_probes(r);
+  return rc;
+}
+
+int kpm_run_total_steps(kpm_run *r) { return r ? r->total_steps : 0; }
+
+int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
+  KPM_CHECK_ARG(r, "run is NULL");
+  KPM_CHECK_ARG(r->have_probes, "probes not set");
+  cudaStream_t st = r->g->ctx->stream;
+  for (int32_t s = 0; s < steps && r->done_steps < r->total_steps; ++s) {
+    const bool first = r->k_index == 0;
+    StepParams p = base_params(r);
+    p.X = r->cur;
+    p.Xprev = r->prev;
+    double *dst = first ? r->b : r->prev;  // T_{k+1} overwrites T_{k-1}
+    p.Y = dst;
+    p.ldos_col = r->k_index + 1;
+    KPM_CUDA(launch_step(r, p, false, first, st));
+    const int m = r->k_index + 1;
+    if (r->mode == KPM_MODE_DOS_DOUBLING) KPM_CUDA(launch_finalize(r, 2, m, st));
+    else if (r->mode == KPM_MODE_DOS_DIRECT) KPM_CUDA(launch_finalize(r, 1, m, st));
+    r->prev = r->cur;
+    r->cur = dst;
+    r->k_index += 1;
+    r->done_steps += 1;
+  }
+  if (remaining) *remaining = r->total_steps - r->done_steps;
+  return KPM_OK;
+}
+
+int kpm_run_result(kpm_run *r, double *out, double trace_scale, int64_t *bad_node) {
+  KPM_CHECK_ARG(r && out, "bad arguments");
+  KPM_CHECK_ARG(r->have_probes, "probes not set");
+  KPM_CHECK_ARG(r->done_steps == r->total_steps, "run not finished (%d of %d steps)",
+                r->done_steps, r->total_steps);
+  cudaStream_t st = r->g->ctx->stream;
+  KPM_CUDA(cudaSetDevice(r->g->ctx->device));
+  int32_t hflag[4];
+  KPM_CUDA(cudaMemcpyAsync(hflag, r->flag, sizeof(hflag), cudaMemcpyDeviceToHost, st));
+  if (r->mode == KPM_MODE_LDOS) {
+    KPM_CUDA(cudaStreamSynchronize(st));
+    if (hflag[0]) {
+      set_error("Chebyshev recurrence overflowed; re-estimate the spectral range "
+                "with a larger margin");
+      return KPM_ENONFINITE;
+    }
+    if (!(r->flags & KPM_LDOS_RAW) && hflag[1] != 0x7fffffff) {
+      if (bad_node) *bad_node = hflag[1];
+      set_error("zero probe mass at node %d; its moments are unrecoverable", hflag[1]);
+      return KPM_EZEROMASS;
+    }
+    if (r->g->n > 0)
+      ldos_finish<<<grid_of(r->g->n * (r->m_max + 1)), 256, 0, st>>>(
+          r->ldos, r->den, r->g->n, r->m_max + 1, (r->flags & KPM_LDOS_RAW) != 0,
+          trace_scale);
+    KPM_CUDA(cudaGetLastError());
+    r->have_probes = false;  // the num buffer now holds values
+    if (r->g->n > 0)
+      KPM_CUDA(cudaMemcpyAsync(out, r->ldos,
+                               sizeof(double) * (size_t)r->g->n * (r->m_max + 1),
+                               cudaMemcpyDefault, st));
+    KPM_CUDA(cudaStreamSynchronize(st));
+    return KPM_OK;
+  }
+  KPM_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * r->k, r->contrib, sizeof(double) * r->ld,
+                             sizeof(double) * r->k, r->m_max + 1, cudaMemcpyDefault, st));
+  KPM_CUDA(cudaStreamSynchronize(st));
+  return KPM_OK;
+}
+
+int kpm_run_block(kpm_run *r, const double **t_k, int64_t *ld, int32_t *k_index) {
+  KPM_CHECK_ARG(r, "run is NULL");
+  if (t_k) *t_k = r->cur;
+  if (ld) *ld = r->ld;
+  if (k_index) *k_index = r->k_index;
+  return KPM_OK;
+}
+
+void kpm_run_free(kpm_run *r) {
+  if (!r) return;
+  cudaSetDevice(r->g->ctx->device);
+  cudaStreamSynchronize(r->g->ctx->stream);
+  cudaFree(r->a);
+  cudaFree(r->b);
+  cudaFree(r->z);
+  cudaFree(r->partial);
+  cudaFree(r->contrib);
+  cudaFree(r->ldos);
+  cudaFree(r->den);
+  cudaFree(r->flag);
+  delete r;
+}
+
+int kpm_dos_contrib(kpm_graph *g, const double *z, int64_t k, int32_t m_max,
+                    int32_t doubling, double *contrib) {
+  kpm_run *r = nullptr;
+  KPM_TRY(kpm_run_create(g, k, doubling ? KPM_MODE_DOS_DOUBLING : KPM_MODE_DOS_DIRECT,
+                         m_max, 0, &r));
+  int rc = kpm_run_set_probes(r, z, k);
+  if (rc == KPM_OK) rc = kpm_run_advance(r, r->total_steps, nullptr);
+  if (rc == KPM_OK) rc = kpm_run_result(r, contrib, 0.0, nullptr);
+  kpm_run_free(r);
+  return rc;
+}
+
+int kpm_ldos(kpm_graph *g, const double *z, int64_t k, int32_t m_max, int32_t flags,
+             double trace_scale, double *values, int64_t *bad_node) {
+  kpm_run *r = nullptr;
+  KPM_TRY(kpm_run_create(g, k, KPM_MODE_LDOS, m_max, flags, &r));
+  int rc = kpm_run_set_probes(r, z, k);
+  if (rc == KPM_OK) rc = kpm_run_advance(r, r->total_steps, nullptr);
+  if (rc == KPM_OK) rc = kpm_run_result(r, values, trace_scale, bad_node);
+  kpm_run_free(r);
+  return rc;
+}
+
+int kpm_probes_rademacher(kpm_ctx *ctx, int64_t n, int64_t ncols, const uint64_t *keys,
+                          double *z, int64_t ldz, int64_t col0) {
+  KPM_CHECK_ARG(ctx && keys && z && n >= 0 && ncols >= 0 && col0 >= 0 && ldz >= col0 + ncols,
+                "bad arguments");
+  KPM_CHECK_ARG(is_device_ptr(z), "z must be a device buffer");
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  DevBuf tk;
+  const void *dk;
+  KPM_TRY(stage_in(ctx->stream, keys, sizeof(uint64_t) * 2 * ncols, tk, &dk));
+  if (n > 0 && ncols > 0)
+    rademacher_kernel<<<grid_of(((n + 7) / 8) * ncols), 256, 0, ctx->stream>>>(
+        n, ncols, (const uint64_t *)dk, z, ldz, col0);
+  KPM_CUDA(cudaGetLastError());
+  KPM_CUDA(cudaStreamSynchronize(ctx->stream));  // tk is freed on return
+  return KPM_OK;
+}
+
+int kpm_csr_matvec(kpm_ctx *ctx, int64_t n_rows, const int64_t *indptr,
+                   const int64_t *indices, const double *data, int64_t nnz,
+                   const double *x, int64_t n_x_rows, int64_t k, double *out) {
+  KPM_CHECK_ARG(ctx && n_rows >= 0 && nnz >= 0 && k >= 0 && n_x_rows >= 0, "bad arguments");
+  KPM_CHECK_ARG(indptr && (nnz == 0 || (indices && data)), "NULL CSR arrays");
+  if (n_rows == 0 || k == 0) return KPM_OK;
+  KPM_CHECK_ARG(out && (x || n_x_rows == 0), "NULL x/out");
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  DevBuf tp, ti, td, tx, to;
+  const void *dp, *di, *dd, *dx;
+  KPM_TRY(stage_in(st, indptr, sizeof(int64_t) * (n_rows + 1), tp, &dp));
+  KPM_TRY(stage_in(st, indices, sizeof(int64_t) * nnz, ti, &di));
+  KPM_TRY(stage_in(st, data, sizeof(double) * nnz, td, &dd));
+  KPM_TRY(stage_in(st, x, sizeof(double) * n_x_rows * k, tx, &dx));
+  double *dout = out;
+  const bool out_dev = is_device_ptr(out);
+  if (!out_dev) {
+    KPM_CUDA(cudaMalloc(&to.ptr, sizeof(double) * n_rows * k));
+    dout = (double *)to.ptr;
+  }
+  const int64_t warps = n_rows;
+  csr_matvec_kernel<<<grid_of(warps * 32), 256, 0, st>>>(
+      n_rows, (const int64_t *)dp, (const int64_t *)di, (const double *)dd,
+      (const double *)dx, k, dout);
+  KPM_CUDA(cudaGetLastError());
+  if (!out_dev)
+    KPM_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * n_rows * k, cudaMemcpyDeviceToHost, st));
+  KPM_CUDA(cudaStreamSynchronize(st));
+  return KPM_OK;
+}
+
+int kpm_filter_probes(kpm_ctx *ctx, int64_t n, int64_t k, double *z, int64_t ldz,
+                      int64_t n_groups, const int64_t *group_ptr, const int64_t *vec_ptr,
+                      const int64_t *vec_idx, const double *vec_val) {
+  KPM_CHECK_ARG(ctx && z && n >= 0 && k >= 0 && ldz >= k && n_groups >= 0, "bad arguments");
+  if (n_groups == 0 || k == 0 || n == 0) return KPM_OK;
+  KPM_CHECK_ARG(group_ptr && vec_ptr && vec_idx && vec_val, "NULL vector arrays");
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  // group_ptr / vec_ptr are read on the host for the sizes
+  int64_t nvec = 0, nent = 0;
+  const bool gp_dev = is_device_ptr(group_ptr);
+  if (gp_dev) {
+    KPM_CUDA(cudaMemcpy(&nvec, group_ptr + n_groups, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  } else {
+    nvec = group_ptr[n_groups];
+  }
+  if (is_device_ptr(vec_ptr)) {
+    KPM_CUDA(cudaMemcpy(&nent, vec_ptr + nvec, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  } else {
+    nent = vec_ptr[nvec];
+  }
+  DevBuf tg, tv, ti, tw, tz;
+  const void *dg, *dv, *di, *dw;
+  KPM_TRY(stage_in(st, group_ptr, sizeof(int64_t) * (n_groups + 1), tg, &dg));
+  KPM_TRY(stage_in(st, vec_ptr, sizeof(int64_t) * (nvec + 1), tv, &dv));
+  KPM_TRY(stage_in(st, vec_idx, sizeof(int64_t) * nent, ti, &di));
+  KPM_TRY(stage_in(st, vec_val, sizeof(double) * nent, tw, &dw));
+  double *dz = z;
+  const bool z_dev = is_device_ptr(z);
+  if (!z_dev) {
+    KPM_CUDA(cudaMalloc(&tz.ptr, sizeof(double) * n * ldz));
+    KPM_CUDA(cudaMemcpyAsync(tz.ptr, z, sizeof(double) * n * ldz, cudaMemcpyHostToDevice, st));
+    dz = (double *)tz.ptr;
+  }
+  filter_kernel<<<grid_of(n_groups * 32), 256, 0, st>>>(
+      dz, k, ldz, n_groups, (const int64_t *)dg, (const int64_t *)dv, (const int64_t *)di,
+      (const double *)dw);
+  KPM_CUDA(cudaGetLastError());
+  if (!z_dev)
+    KPM_CUDA(cudaMemcpyAsync(z, dz, sizeof(double) * n * ldz, cudaMemcpyDeviceToHost, st));
+  KPM_CUDA(cudaStreamSynchronize(st));
+  return KPM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+"""Probe sharding across GPUs: one process per GPU.
+
+Probe columns are independent units: rank r of N takes the contiguous column
+range [r*P/N, (r+1)*P/N), the CSR is replicated on every GPU, and the only
+exchange is ONE all-reduce (sum, fp64) of the zero-padded (M+1) x P
+per-probe contribution matrix -- every column is written by exactly one rank,
+so the sum is exact and the host finishes identically to 1 GPU.  LDOS sums
+per-node numerators with one all-reduce of the (n, M+1) block.
+
+torch.distributed (NCCL on B200, gloo in the CPU tests) is plumbing only.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import RecurrenceBlowupError
+from .kpm import _BLOWUP, MODE_GLOBAL, MODE_PER_NODE, ChebMoments
+
+
+def shard_range(nz: int, rank: int, world: int):
+    """Contiguous, balanced column range of `rank` (sizes differ by <= 1)."""
+    base, extra = divmod(nz, world)
+    c0 = rank * base + min(rank, extra)
+    return c0, c0 + base + (1 if rank < extra else 0)
+
+
+def _allreduce_sum(arr: np.ndarray, group=None) -> np.ndarray:
+    import torch
+    import torch.distributed as dist
+
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        t = torch.from_numpy(arr).cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return t.cpu().numpy()
+    t = torch.from_numpy(arr)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t.numpy()
+
+
+def _world(group):
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def combine_contrib(local: np.ndarray, c0: int, nz: int, group=None) -> np.ndarray:
+    """Zero-pad this rank's (M+1) x (c1-c0) block into (M+1) x nz and sum."""
+    full = np.zeros((local.shape[0], nz))
+    full[:, c0:c0 + local.shape[1]] = local
+    _, world = _world(group)
+    return _allreduce_sum(full, group) if world > 1 else full
+
+
+def dos_moments_sharded(sop, probes, m_max, effective_dim=None, doubling=True,
+                        group=None, contrib_fn=None) -> ChebMoments:
+    """dos_moments with probe columns sharded over the process group."""
+    rank, world = _world(group)
+    c0, c1 = shard_range(probes.nz, rank, world)
+    if contrib_fn is None:
+        from .kpm import dos_contrib as contrib_fn
+    local = contrib_fn(sop, probes.column_slice(c0, c1), m_max, doubling=doubling) \
+        if c1 > c0 else np.zeros((m_max + 1, 0))
+    contrib = combine_contrib(local, c0, probes.nz, group)
+    if not np.all(np.isfinite(contrib)):
+        raise RecurrenceBlowupError(_BLOWUP)
+    denom = float(effective_dim) if effective_dim is not None else float(sop.n)
+    values = contrib.sum(axis=1) * (probes.trace_scale / denom)
+    return ChebMoments(mode=MODE_GLOBAL, values=values, scale_map=sop.scale_map,
+                       probe_meta=probes.meta())
+
+
+def pdos_moments_sharded(sop, probes, m_max, normalized=True, group=None,
+                         num_fn=None) -> ChebMoments:
+    """pdos_moments with probe columns sharded: per-node raw sums all-reduced."""
+    rank, world = _world(group)
+    c0, c1 = shard_range(probes.nz, rank, world)
+    if num_fn is None:
+        from .kpm import pdos_num as num_fn
+    local = num_fn(sop, probes.column_slice(c0, c1), m_max) if c1 > c0 \
+        else np.zeros((sop.n, m_max + 1))
+    num = _allreduce_sum(np.ascontiguousarray(local), group) if world > 1 else local
+    if not np.all(np.isfinite(num)):
+        raise RecurrenceBlowupError(_BLOWUP)
+    if normalized:
+        den = num[:, 0].copy()
+        if np.any(den == 0.0):
+            k = int(np.argmax(den == 0.0))
+            raise ValueError(f"zero probe mass at node {k}; its moments are unrecoverable")
+        values = num / den[:, None]
+    else:
+        values = num * probes.trace_scale
+    return ChebMoments(mode=MODE_PER_NODE, values=np.ascontiguousarray(values),
+                       scale_map=sop.scale_map, probe_meta=probes.meta())
