@@ -153,6 +153,12 @@ int kpm_run_set_rademacher(kpm_run *r, const uint64_t *keys);
  * reduction) plus one deterministic finalize kernel. */
 int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining);
 int kpm_run_total_steps(kpm_run *r);
+/* Kernel timing for the roofline: when enabled, kpm_run_advance brackets
+ * every fused step kernel with CUDA events on the context stream;
+ * kpm_run_kernel_time synchronises and returns the summed milliseconds and
+ * the launch count since the last reset. */
+int kpm_run_set_timing(kpm_run *r, int enable);
+int kpm_run_kernel_time(kpm_run *r, double *ms, int32_t *launches);
 /* Global modes: contrib (m_max+1) x k, contrib[m][j] = z_j^T T_m z_j
  * (kpm.py:107-108).  LDOS: values n x (m_max+1) = (num/den).T (kpm.py:148),
  * or num*trace_scale with KPM_LDOS_RAW.  `out` host-or-device.  Returns

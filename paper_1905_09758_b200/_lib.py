@@ -73,6 +73,8 @@ SIGNATURES = {
     "kpm_run_set_rademacher": (_c_int, [_c_vp, _c_vp]),
     "kpm_run_advance": (_c_int, [_c_vp, _c_i32, ctypes.POINTER(_c_i32)]),
     "kpm_run_total_steps": (_c_int, [_c_vp]),
+    "kpm_run_set_timing": (_c_int, [_c_vp, _c_int]),
+    "kpm_run_kernel_time": (_c_int, [_c_vp, ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_i32)]),
     "kpm_run_result": (_c_int, [_c_vp, _c_vp, _c_dbl, ctypes.POINTER(_c_i64)]),
     "kpm_run_block": (_c_int, [_c_vp, _PP, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i32)]),
     "kpm_run_free": (None, [_c_vp]),

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/kpm.h"
 
@@ -92,4 +93,8 @@ struct kpm_run {
   double *ldos = nullptr;     // n x (m_max+1) (LDOS)
   double *den = nullptr;      // n (LDOS)
   int32_t *flag = nullptr;    // [0]: non-finite seen; [1..2]: zero-mass node
+  // optional per-launch timing of the step kernel (roofline evidence)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // pairs (start, stop), reused
+  int32_t ev_used = 0;
 };

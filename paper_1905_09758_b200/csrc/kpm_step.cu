@@ -605,7 +605,18 @@ int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
     double *dst = first ? r->b : r->prev;  // T_{k+1} overwrites T_{k-1}
     p.Y = dst;
     p.ldos_col = r->k_index + 1;
+    if (r->timing) {
+      if ((size_t)(2 * r->ev_used + 2) > r->ev.size()) {
+        for (int q = 0; q < 2; ++q) {
+          cudaEvent_t e;
+          KPM_CUDA(cudaEventCreate(&e));
+          r->ev.push_back(e);
+        }
+      }
+      KPM_CUDA(cudaEventRecord(r->ev[2 * r->ev_used], st));
+    }
     KPM_CUDA(launch_step(r, p, false, first, st));
+    if (r->timing) KPM_CUDA(cudaEventRecord(r->ev[2 * r->ev_used++ + 1], st));
     const int m = r->k_index + 1;
     if (r->mode == KPM_MODE_DOS_DOUBLING) KPM_CUDA(launch_finalize(r, 2, m, st));
     else if (r->mode == KPM_MODE_DOS_DIRECT) KPM_CUDA(launch_finalize(r, 1, m, st));
@@ -678,7 +689,30 @@ void kpm_run_free(kpm_run *r) {
   cudaFree(r->ldos);
   cudaFree(r->den);
   cudaFree(r->flag);
+  for (cudaEvent_t e : r->ev) cudaEventDestroy(e);
   delete r;
+}
+
+int kpm_run_set_timing(kpm_run *r, int enable) {
+  KPM_CHECK_ARG(r, "run is NULL");
+  r->timing = enable != 0;
+  r->ev_used = 0;
+  return KPM_OK;
+}
+
+int kpm_run_kernel_time(kpm_run *r, double *ms, int32_t *launches) {
+  KPM_CHECK_ARG(r && ms, "bad arguments");
+  KPM_CUDA(cudaStreamSynchronize(r->g->ctx->stream));
+  double tot = 0.0;
+  for (int32_t i = 0; i < r->ev_used; ++i) {
+    float t = 0.f;
+    KPM_CUDA(cudaEventElapsedTime(&t, r->ev[2 * i], r->ev[2 * i + 1]));
+    tot += t;
+  }
+  *ms = tot;
+  if (launches) *launches = r->ev_used;
+  r->ev_used = 0;
+  return KPM_OK;
 }
 
 int kpm_dos_contrib(kpm_graph *g, const double *z, int64_t k, int32_t m_max,

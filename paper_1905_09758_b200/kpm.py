@@ -126,6 +126,15 @@ class Run:
                                               ctypes.byref(bad)), "run_result")
         return out
 
+    def set_timing(self, enable=True):
+        _lib.check(_lib.load().kpm_run_set_timing(self._h, 1 if enable else 0))
+
+    def kernel_time(self):
+        """(summed step-kernel milliseconds, launches) since the last call."""
+        ms, n = ctypes.c_double(), ctypes.c_int32()
+        _lib.check(_lib.load().kpm_run_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
     def block(self):
         """(device pointer of T_k, row stride, k) for bit-exactness checks."""
         p, ld, ki = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int32()
