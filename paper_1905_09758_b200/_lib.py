@@ -17,7 +17,7 @@ import numpy as np
 from .errors import NetdosError, RecurrenceBlowupError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkpm.so")
+LIB_PATH = os.environ.get("KPM_LIB") or os.path.join(HERE, "libkpm.so")
 
 KPM_OK = 0
 KPM_EINVAL = -1

@@ -16,7 +16,13 @@
 // atomics, so the CSR is deterministic and bit-identical to the reference.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
 
 #include "kpm_internal.cuh"
 
@@ -160,11 +166,24 @@ __global__ void dinv_kernel(const int64_t *__restrict__ row_ptr, int64_t n,
   if ((threadIdx.x & 31) == 0) atomicMax(max_deg, local);
 }
 
-// Chunk c covers rows [start[c], start[c+1]); boundaries split the prefix
-// cost row_ptr[i] + kRowCost*i evenly.  Depends on the graph only.
+// Chunk c covers rows [start[c], start[c+1]); boundaries split the prefix of
+// the per-row cost min(deg, heavy) + kRowCost evenly (heavy rows are worked
+// by their own CTAs, kpm_step.cu).  Depends on the graph only.
 static constexpr int64_t kRowCost = 8;
 
-__global__ void chunk_bounds(const int64_t *__restrict__ row_ptr, int64_t n,
+__global__ void row_cost_kernel(const int64_t *__restrict__ row_ptr, int64_t n,
+                                int64_t heavy, int64_t *__restrict__ cost,
+                                int32_t *__restrict__ is_heavy) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t d = row_ptr[i + 1] - row_ptr[i];
+    bool h = d >= heavy;
+    cost[i] = (h ? 0 : d) + kRowCost;
+    is_heavy[i] = h ? 1 : 0;
+  }
+}
+
+__global__ void chunk_bounds(const int64_t *__restrict__ prefix, int64_t n,
                              int32_t n_chunks, int64_t target,
                              int32_t *__restrict__ start) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -172,12 +191,20 @@ __global__ void chunk_bounds(const int64_t *__restrict__ row_ptr, int64_t n,
   if (c == 0) { start[0] = 0; return; }
   if (c == n_chunks) { start[c] = (int32_t)n; return; }
   int64_t want = (int64_t)c * target;
-  int64_t lo = 0, hi = n;  // first i with cost(i) >= want
+  int64_t lo = 0, hi = n;  // first i with prefix(i) >= want
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
-    if (row_ptr[mid] + kRowCost * mid >= want) hi = mid; else lo = mid + 1;
+    if (prefix[mid] >= want) hi = mid; else lo = mid + 1;
   }
   start[c] = (int32_t)lo;
+}
+
+__global__ void gather_degrees(const int64_t *__restrict__ row_ptr,
+                               const int32_t *__restrict__ rows, int64_t k,
+                               int64_t *__restrict__ deg) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < k;
+       t += (int64_t)gridDim.x * blockDim.x)
+    deg[t] = row_ptr[rows[t] + 1] - row_ptr[rows[t]];
 }
 
 static int grid_for(int64_t work, int threads = 256) {
@@ -189,27 +216,97 @@ static int grid_for(int64_t work, int threads = 256) {
 
 int finish_graph(kpm_graph *g) {
   cudaStream_t st = g->ctx->stream;
+  const int64_t n = g->n;
   unsigned long long *dmax = nullptr;
   KPM_CUDA(cudaMallocAsync(&dmax, sizeof(unsigned long long), st));
   KPM_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
-  if (g->n > 0)
-    dinv_kernel<<<grid_for(g->n), 256, 0, st>>>(g->row_ptr, g->n, g->dinv, dmax);
+  if (n > 0)
+    dinv_kernel<<<grid_for(n), 256, 0, st>>>(g->row_ptr, n, g->dinv, dmax);
   unsigned long long hmax = 0;
   KPM_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof(hmax), cudaMemcpyDeviceToHost, st));
   KPM_CUDA(cudaFreeAsync(dmax, st));
-  // schedule: a fixed denominator (148 SMs x 32) keeps chunks independent of
-  // the device and of the probe count, so reductions are reproducible.
-  int64_t total = g->nnz + kRowCost * g->n;
-  int64_t target = (total + 148 * 32 - 1) / (148 * 32);
+
+  // capped row costs -> prefix (n+1) ; heavy-row flags
+  g->heavy_threshold = kHeavyDegree;
+  if (const char *e = getenv("KPM_HEAVY_DEGREE")) {  // tests force the hub path
+    long long v = atoll(e);
+    if (v > 0) g->heavy_threshold = v;
+  }
+  int64_t *prefix = nullptr;
+  int32_t *flags = nullptr;
+  KPM_CUDA(cudaMalloc(&prefix, sizeof(int64_t) * (n + 1)));
+  KPM_CUDA(cudaMalloc(&flags, sizeof(int32_t) * (n > 0 ? n : 1)));
+  KPM_CUDA(cudaMemsetAsync(prefix, 0, sizeof(int64_t) * (n + 1), st));
+  if (n > 0) {
+    row_cost_kernel<<<grid_for(n), 256, 0, st>>>(g->row_ptr, n, g->heavy_threshold, prefix,
+                                                 flags);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, prefix, prefix, n + 1, st);
+    void *tmp = nullptr;
+    KPM_CUDA(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, prefix, prefix, n + 1, st);
+    KPM_CUDA(cudaGetLastError());
+    KPM_CUDA(cudaFreeAsync(tmp, st));
+  }
+  int64_t total = 0;
+  KPM_CUDA(cudaMemcpyAsync(&total, prefix + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  KPM_CUDA(cudaStreamSynchronize(st));
+  // a fixed denominator (148 SMs x 128) keeps chunks independent of the device
+  // and of the probe count, so reductions are reproducible.
+  int64_t target = (total + 148 * 128 - 1) / (148 * 128);
   if (target < 256) target = 256;
   int64_t nch = (total + target - 1) / target;
   if (nch < 1) nch = 1;
   g->n_chunks = (int32_t)nch;
   KPM_CUDA(cudaMalloc(&g->chunk_start, sizeof(int32_t) * (nch + 1)));
-  chunk_bounds<<<(int)((nch + 1 + 255) / 256), 256, 0, st>>>(
-      g->row_ptr, g->n, g->n_chunks, target, g->chunk_start);
+  chunk_bounds<<<(int)((nch + 1 + 255) / 256), 256, 0, st>>>(prefix, n, g->n_chunks, target,
+                                                               g->chunk_start);
   KPM_CUDA(cudaGetLastError());
+
+  // heavy rows, ordered by (degree desc, row asc): deterministic, graph-only
+  g->n_heavy = 0;
+  if (n > 0 && (int64_t)hmax >= g->heavy_threshold) {
+    int32_t *sel = nullptr, *dnum = nullptr;
+    KPM_CUDA(cudaMalloc(&sel, sizeof(int32_t) * n));
+    KPM_CUDA(cudaMalloc(&dnum, sizeof(int32_t)));
+    size_t tb = 0;
+    thrust::counting_iterator<int32_t> rows(0);
+    cub::DeviceSelect::Flagged(nullptr, tb, rows, flags, sel, dnum, (int)n, st);
+    void *tmp = nullptr;
+    KPM_CUDA(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceSelect::Flagged(tmp, tb, rows, flags, sel, dnum, (int)n, st);
+    KPM_CUDA(cudaGetLastError());
+    KPM_CUDA(cudaFreeAsync(tmp, st));
+    int32_t nh = 0;
+    KPM_CUDA(cudaMemcpyAsync(&nh, dnum, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    KPM_CUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> hrows(nh);
+    std::vector<int64_t> hdeg(nh);
+    if (nh > 0) {
+      int64_t *ddeg = nullptr;
+      KPM_CUDA(cudaMalloc(&ddeg, sizeof(int64_t) * nh));
+      gather_degrees<<<grid_for(nh), 256, 0, st>>>(g->row_ptr, sel, nh, ddeg);
+      KPM_CUDA(cudaMemcpyAsync(hrows.data(), sel, sizeof(int32_t) * nh, cudaMemcpyDeviceToHost, st));
+      KPM_CUDA(cudaMemcpyAsync(hdeg.data(), ddeg, sizeof(int64_t) * nh, cudaMemcpyDeviceToHost, st));
+      KPM_CUDA(cudaStreamSynchronize(st));
+      cudaFree(ddeg);
+      std::vector<int32_t> order(nh);
+      for (int32_t t = 0; t < nh; ++t) order[t] = t;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int32_t a, int32_t b) { return hdeg[a] > hdeg[b]; });
+      std::vector<int32_t> sorted(nh);
+      for (int32_t t = 0; t < nh; ++t) sorted[t] = hrows[order[t]];
+      KPM_CUDA(cudaMalloc(&g->heavy_rows, sizeof(int32_t) * nh));
+      KPM_CUDA(cudaMemcpy(g->heavy_rows, sorted.data(), sizeof(int32_t) * nh,
+                          cudaMemcpyHostToDevice));
+    }
+    g->n_heavy = nh;
+    cudaFree(sel);
+    cudaFree(dnum);
+  }
   KPM_CUDA(cudaStreamSynchronize(st));
+  cudaFree(prefix);
+  cudaFree(flags);
   g->max_degree = (int64_t)hmax;
   return KPM_OK;
 }
@@ -472,6 +569,7 @@ void kpm_graph_free(kpm_graph *g) {
   cudaFree(g->dinv);
   cudaFree(g->values);
   cudaFree(g->chunk_start);
+  cudaFree(g->heavy_rows);
   delete g;
 }
 

@@ -74,7 +74,15 @@ struct kpm_graph {
   // load-balanced schedule (depends on the graph only, never on k)
   int32_t n_chunks = 0;
   int32_t *chunk_start = nullptr;  // n_chunks+1 row boundaries
+  // rows with degree >= heavy_threshold are split over column slices and
+  // worked by dedicated warps (degree-desc order); chunks skip them
+  int64_t heavy_threshold = 0;
+  int32_t n_heavy = 0;
+  int32_t *heavy_rows = nullptr;
 };
+
+// degree from which a row is a "heavy" (hub) row (graph-only constant)
+static constexpr int64_t kHeavyDegree = 4096;
 
 struct kpm_run {
   kpm_graph *g = nullptr;
@@ -92,6 +100,10 @@ struct kpm_run {
   double *contrib = nullptr;  // (m_max+1) x ld (global modes)
   double *ldos = nullptr;     // n x (m_max+1) (LDOS)
   double *den = nullptr;      // n (LDOS)
+  double *hpart = nullptr;    // n_heavy x 2 x ld (global modes)
+  double *hldos = nullptr;    // n_heavy x slices (LDOS)
+  double *gpart = nullptr;    // chunk-group partials (level-1 reduction)
+  unsigned long long *queue = nullptr;  // persistent-kernel work counter
   int32_t *flag = nullptr;    // [0]: non-finite seen; [1..2]: zero-mass node
   // optional per-launch timing of the step kernel (roofline evidence)
   bool timing = false;

@@ -51,7 +51,149 @@ struct StepParams {
   const int32_t *chunk_start;
   double *partial;         // n_chunks x 2 x ld
   int32_t *flag;
+  // heavy (hub) rows: column-sliced tasks at the head of the work queue
+  const int32_t *heavy_rows;
+  int32_t n_heavy;
+  int64_t n_heavy_tasks;
+  int64_t heavy_threshold;
+  int32_t n_chunks;
+  unsigned long long *queue;  // work-queue counter (zeroed before each launch)
+  double *hpart;           // n_heavy x 2 x ld (global modes)
+  double *hldos;           // n_heavy x n_slices (LDOS)
 };
+
+// Heavy rows are cut into 16-column slices; one warp owns one (row, slice)
+// task.  Lane (nb = lane/4, cg = lane%4) gathers 4 columns of neighbour nb of
+// an 8-neighbour wave, forms the products h_ij * X[j, c] in parallel, and the
+// products are then added IN NEIGHBOUR ORDER through shuffles, so every
+// (row, column) sum keeps the reference's sequential order (bit-exact) while
+// 32 neighbours' gathers are in flight per warp and a hub's slices run on
+// different SMs.
+constexpr int kSlice = 16;
+
+__device__ __forceinline__ void ld4_masked(const double *p, int64_t avail, bool vec,
+                                           double (&v)[4]) {
+  if (vec) {
+    double2 t0 = __ldg(reinterpret_cast<const double2 *>(p));
+    double2 t1 = __ldg(reinterpret_cast<const double2 *>(p + 2));
+    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = c < avail ? __ldg(p + c) : 0.0;
+  }
+}
+
+__device__ __forceinline__ void ld4_rw_masked(const double *p, int64_t avail, bool vec,
+                                              double (&v)[4]) {
+  if (vec) {
+    double2 t0 = *reinterpret_cast<const double2 *>(p);
+    double2 t1 = *reinterpret_cast<const double2 *>(p + 2);
+    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = c < avail ? p[c] : 0.0;
+  }
+}
+
+template <int MODE, bool EXPL, bool FIRST>
+__device__ __forceinline__ void heavy_task(const StepParams &p, int64_t t) {
+  const int lane = threadIdx.x & 31;
+  const int nb = lane >> 2, cg = lane & 3;
+  const int64_t ld = p.ld;
+  const int nsl = (int)((ld + kSlice - 1) / kSlice);
+  const int h = (int)(t / nsl), sl = (int)(t % nsl);
+  const int i = p.heavy_rows[h];
+  const int64_t beg = p.row_ptr[i], end = p.row_ptr[i + 1];
+  double di = 0.0;
+  if constexpr (!EXPL) di = p.dinv[i];
+  const int64_t c0 = (int64_t)sl * kSlice + cg * 4;
+  const int64_t avail = ld - c0;  // columns of this lane inside the row
+  const bool active = avail > 0;
+  const bool vec = (ld & 3) == 0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t base = beg; base < end; base += 32) {
+    const int cnt = (int)min((int64_t)32, end - base);
+    int jl = 0;
+    double hl = 0.0;
+    if (lane < cnt) {
+      jl = p.col[base + lane];
+      if constexpr (EXPL) hl = p.vals[base + lane];
+      else hl = __dmul_rn(di, __ldg(p.dinv + jl));
+    }
+    double v[4][4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int q = w * 8 + nb;
+      const int j = __shfl_sync(0xffffffffu, jl, q);
+      const double hv = __shfl_sync(0xffffffffu, hl, q);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[w][c] = 0.0;
+      if (q < cnt && active) ld4_masked(p.X + (size_t)j * ld + c0, avail, vec, v[w]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[w][c] = __dmul_rn(hv, v[w][c]);
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (w * 8 + u < cnt) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            acc[c] = __dadd_rn(acc[c], __shfl_sync(0xffffffffu, v[w][c], u * 4 + cg));
+        }
+      }
+    }
+  }
+  // epilogue on lanes 0..3 (every lane holds the same sums for its cg)
+  double part = 0.0;
+  if (nb == 0 && active) {
+    const size_t off = (size_t)i * ld + c0;
+    double y[4], xo[4], pv[4], zv[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) y[c] = acc[c];
+    if constexpr (EXPL || MODE == MODE_DBL) ld4_masked(p.X + off, avail, vec, xo);
+    if constexpr (EXPL) {
+      if (p.shift != 0.0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) y[c] = __dsub_rn(y[c], __dmul_rn(p.shift, xo[c]));
+      }
+      if (p.scale != 1.0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) y[c] = __ddiv_rn(y[c], p.scale);
+      }
+    }
+    if constexpr (!FIRST) {
+      ld4_rw_masked(p.Xprev + off, avail, vec, pv);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) y[c] = __dsub_rn(__dmul_rn(2.0, y[c]), pv[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < avail) p.Y[off + c] = y[c];
+    if constexpr (MODE != MODE_DBL) ld4_masked(p.Z + off, avail, vec, zv);
+    double *hp = p.hpart + (size_t)h * 2 * ld + c0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c < avail) {
+        if constexpr (MODE == MODE_DBL) {
+          hp[c] = __dmul_rn(y[c], xo[c]);
+          hp[ld + c] = __dmul_rn(y[c], y[c]);
+        } else if constexpr (MODE == MODE_DIRECT) {
+          hp[c] = __dmul_rn(zv[c], y[c]);
+        } else {
+          part = __dadd_rn(part, __dmul_rn(zv[c], y[c]));
+        }
+      }
+    }
+  }
+  if constexpr (MODE == MODE_LDOS) {
+    // slice sum over the 4 column groups in order (lanes 0..3)
+    double tot = __shfl_sync(0xffffffffu, part, 0);
+#pragma unroll
+    for (int g2 = 1; g2 < 4; ++g2) tot = __dadd_rn(tot, __shfl_sync(0xffffffffu, part, g2));
+    if (lane == 0) p.hldos[(size_t)h * nsl + sl] = tot;
+  }
+}
 
 template <int C>
 __device__ __forceinline__ void ld_vec(const double *p, double (&v)[C]) {
@@ -101,37 +243,43 @@ __device__ __forceinline__ double warp_sum_fixed(double x) {
   return x;
 }
 
-// INIT: step-0 reductions (mu_0 = z.z per probe; LDOS den and column 0).
+// One light row chunk, worked by one warp: rows in order, one row at a time
+// (lane l owns columns [l*C, l*C+C) of each 32*C-wide tile), per-warp moment
+// accumulators in shared memory, written to the chunk's own partial slot.
 template <int C, int MODE, bool EXPL, bool FIRST, bool INIT, int U>
-__global__ void __launch_bounds__(256)
-kpm_step_kernel(const StepParams p) {
-  extern __shared__ double sacc[];  // [W][2][ld] (global modes)
+__device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, double *my) {
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int W = blockDim.x >> 5;
   const int64_t ld = p.ld;
   const int ntiles = (int)((ld + 32 * C - 1) / (32 * C));
-  double *my = sacc + (size_t)warp * 2 * ld;
   if constexpr (MODE != MODE_LDOS) {
     for (int64_t e = lane; e < 2 * ld; e += 32) my[e] = 0.0;
     __syncwarp();
   }
-  const int chunk = blockIdx.x;
   const int r0 = p.chunk_start[chunk], r1 = p.chunk_start[chunk + 1];
-
-  for (int i = r0 + warp; i < r1; i += W) {
+  int64_t beg = 0, end = 0;
+  if constexpr (!INIT) {
+    if (r0 < r1) end = p.row_ptr[r0];
+  }
+  for (int i = r0; i < r1; ++i) {
     const size_t rowoff = (size_t)i * ld;
-    int64_t beg = 0, end = 0;
     double di = 0.0;
     if constexpr (!INIT) {
-      beg = p.row_ptr[i];
+      beg = end;
       end = p.row_ptr[i + 1];
+      if (p.n_heavy > 0 && end - beg >= p.heavy_threshold) continue;  // hub task
       if constexpr (!EXPL) di = p.dinv[i];
     }
     double lsum = 0.0;  // LDOS lane partial
     for (int t = 0; t < ntiles; ++t) {
       const int64_t c0 = ((int64_t)t * 32 + lane) * C;
       const bool active = c0 < ld;
+      double y[C], xo[C], pv[C], zv[C];
+      // own-row operands first: independent of the neighbour walk
+      if (active) {
+        if constexpr (INIT || EXPL || MODE == MODE_DBL) ld_vec<C>(p.X + rowoff + c0, xo);
+        if constexpr (!INIT && !FIRST) ld_vec_rw<C>(p.Xprev + rowoff + c0, pv);
+        if constexpr (!INIT && MODE != MODE_DBL) ld_vec<C>(p.Z + rowoff + c0, zv);
+      }
       double acc[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) acc[c] = 0.0;
@@ -166,13 +314,12 @@ kpm_step_kernel(const StepParams p) {
         }
       }
       if (!active) continue;
-      double y[C], xo[C], pv[C], zv[C];
       if constexpr (INIT) {
-        ld_vec<C>(p.X + rowoff + c0, y);  // T_0 = z
+#pragma unroll
+        for (int c = 0; c < C; ++c) y[c] = zv[c] = xo[c];  // T_0 = z
       } else {
 #pragma unroll
         for (int c = 0; c < C; ++c) y[c] = acc[c];
-        if constexpr (EXPL || MODE == MODE_DBL) ld_vec<C>(p.X + rowoff + c0, xo);
         if constexpr (EXPL) {
           // operators.py:144-147: y -= shift*x; y /= scale (separate roundings)
           if (p.shift != 0.0) {
@@ -185,19 +332,10 @@ kpm_step_kernel(const StepParams p) {
           }
         }
         if constexpr (!FIRST) {
-          ld_vec_rw<C>(p.Xprev + rowoff + c0, pv);
 #pragma unroll
           for (int c = 0; c < C; ++c) y[c] = __dsub_rn(__dmul_rn(2.0, y[c]), pv[c]);
         }
         st_vec<C>(p.Y + rowoff + c0, y);
-      }
-      if constexpr (MODE == MODE_DIRECT || MODE == MODE_LDOS) {
-        if constexpr (INIT) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) zv[c] = y[c];
-        } else {
-          ld_vec<C>(p.Z + rowoff + c0, zv);
-        }
       }
       if constexpr (MODE == MODE_DBL) {
         double *s1 = my + c0, *s2 = my + ld + c0;
@@ -222,7 +360,6 @@ kpm_step_kernel(const StepParams p) {
     if constexpr (MODE == MODE_LDOS) {
       const double num = warp_sum_fixed(lsum);
       if (lane == 0) {
-        const size_t o = (size_t)i * p.ldos_stride + p.ldos_col;
         if (!isfinite(num)) atomicOr(p.flag, 1);
         if constexpr (INIT) {
           // kpm.py:144-147: den = einsum(z, z) (same reduction as num[0])
@@ -230,31 +367,84 @@ kpm_step_kernel(const StepParams p) {
           den[i] = num;
           if (!p.ldos_raw && num == 0.0) atomicMin(p.flag + 1, i);
         }
-        p.ldos[o] = num;  // raw num[m, i]; kpm_run_result applies /den
+        p.ldos[(size_t)i * p.ldos_stride + p.ldos_col] = num;  // raw num[m, i]
       }
     }
   }
   if constexpr (MODE != MODE_LDOS) {
-    __syncthreads();
-    // combine warps in fixed order -> one partial per chunk
+    __syncwarp();
     const int nred = (MODE == MODE_DBL && !INIT) ? 2 : 1;
     double *out = p.partial + (size_t)chunk * 2 * ld;
-    for (int64_t e = threadIdx.x; e < nred * ld; e += blockDim.x) {
-      double s = sacc[e];
-      for (int w = 1; w < W; ++w) s = __dadd_rn(s, sacc[(size_t)w * 2 * ld + e]);
-      out[e] = s;
-    }
+    for (int64_t e = lane; e < nred * ld; e += 32) out[e] = my[e];
+    __syncwarp();
   }
 }
 
-// Sum chunk partials in fixed order and write contrib rows.
+// Persistent fused step kernel.  Work items: [0, n_heavy_tasks) hub-row
+// slices in degree-descending order, then the light row chunks.  Warps grab
+// items from one atomic counter (dynamic load balance, hubs first); every item
+// writes its own partial slot, so the reduction order is fixed by the graph
+// alone -- independent of the schedule, the launch shape and the probe count.
+#ifndef KPM_MIN_BLOCKS
+#define KPM_MIN_BLOCKS 3
+#endif
+#ifndef KPM_U4
+#define KPM_U4 4  // gathers in flight per lane-pair for the 4-column layout
+#endif
+template <int C, int MODE, bool EXPL, bool FIRST, bool INIT, int U>
+__global__ void __launch_bounds__(256, KPM_MIN_BLOCKS)
+kpm_step_kernel(const StepParams p) {
+  extern __shared__ double sacc[];  // [W][2][ld] per-warp accumulators
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double *my = sacc + (size_t)warp * 2 * p.ld;
+  const int64_t n_heavy_tasks = INIT ? 0 : p.n_heavy_tasks;
+  const int64_t total = n_heavy_tasks + p.n_chunks;
+  for (;;) {
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(p.queue, 1ull);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if ((int64_t)item >= total) break;
+    if constexpr (!INIT) {
+      if ((int64_t)item < n_heavy_tasks) {
+        heavy_task<MODE, EXPL, FIRST>(p, (int64_t)item);
+        continue;
+      }
+    }
+    light_chunk<C, MODE, EXPL, FIRST, INIT, U>(p, (int)((int64_t)item - n_heavy_tasks), my);
+  }
+}
+
+// Level 1 of the deterministic reduction: consecutive groups of kGroup chunk
+// partials summed in chunk order.
+constexpr int kGroup = 32;
+
+__global__ void reduce_groups_kernel(const double *__restrict__ partial, int n_chunks,
+                                     int64_t ld, int64_t k, int nred,
+                                     double *__restrict__ gpart) {
+  const int64_t n_groups = (n_chunks + kGroup - 1) / kGroup;
+  const int64_t per = nred * k;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_groups * per;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = t / per, e = t % per;
+    const int red = (int)(e / k);
+    const int64_t c = e % k;
+    const int ch1 = (int)min((int64_t)n_chunks, (g + 1) * kGroup);
+    double s = 0.0;
+    for (int ch = (int)(g * kGroup); ch < ch1; ++ch)
+      s = __dadd_rn(s, partial[(size_t)ch * 2 * ld + red * ld + c]);
+    gpart[(size_t)g * 2 * ld + red * ld + c] = s;
+  }
+}
+
+// Level 2: groups (then hub rows) in fixed order -> contrib rows.
 //   which = 0: INIT       contrib[0] = S1
 //   which = 1: DIRECT     contrib[m] = S1
 //   which = 2: DBL step s contrib[2s-1] = 2 S1 - mu_1 (s==1: S1),
 //                         contrib[2s]   = 2 S2 - mu_0     (if 2s <= M)
-__global__ void finalize_kernel(const double *__restrict__ partial,
-                                int n_chunks, int64_t ld, int64_t k,
-                                int which, int m, int m_max,
+__global__ void finalize_kernel(const double *__restrict__ gpart, int n_groups,
+                                const double *__restrict__ hpart, int n_heavy, int64_t ld,
+                                int64_t k, int which, int m, int m_max,
                                 double *__restrict__ contrib) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -263,16 +453,21 @@ __global__ void finalize_kernel(const double *__restrict__ partial,
   const int red = (int)(gw / k);
   const int64_t c = gw % k;
   double s = 0.0;
-  for (int ch = lane; ch < n_chunks; ch += 32)
-    s = __dadd_rn(s, partial[(size_t)ch * 2 * ld + red * ld + c]);
+  for (int g = lane; g < n_groups; g += 32)
+    s = __dadd_rn(s, gpart[(size_t)g * 2 * ld + red * ld + c]);
   s = warp_sum_fixed(s);
+  if (n_heavy > 0) {  // hub rows after the chunks, in hub-list order
+    double sh = 0.0;
+    for (int hh = lane; hh < n_heavy; hh += 32)
+      sh = __dadd_rn(sh, hpart[(size_t)hh * 2 * ld + red * ld + c]);
+    s = __dadd_rn(s, warp_sum_fixed(sh));
+  }
   if (lane != 0) return;
   if (which == 0) {
     contrib[c] = s;
   } else if (which == 1) {
     contrib[(size_t)m * ld + c] = s;
   } else {
-    // m = step index s >= 1 producing T_s
     if (red == 0) {
       const int row = 2 * m - 1;
       if (row <= m_max)
@@ -285,11 +480,34 @@ __global__ void finalize_kernel(const double *__restrict__ partial,
   }
 }
 
+// LDOS hub rows: sum the per-slice partials in slice order.
+__global__ void ldos_heavy_kernel(const double *__restrict__ hldos, const int32_t *rows,
+                                  int n_heavy, int nsl, double *ldos, int64_t stride,
+                                  int col, int32_t *flag) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= n_heavy) return;
+  double s = hldos[(size_t)h * nsl];
+  for (int q = 1; q < nsl; ++q) s = __dadd_rn(s, hldos[(size_t)h * nsl + q]);
+  if (!isfinite(s)) atomicOr(flag, 1);
+  ldos[(size_t)rows[h] * stride + col] = s;
+}
+
 // ---------------------------------------------------------------- dispatch
+template <typename K>
+static int resident_blocks(K kern, size_t smem) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 256, smem) != cudaSuccess ||
+      nb < 1) {
+    cudaGetLastError();
+    nb = 1;
+  }
+  return nb;
+}
+
 template <int C, int MODE, bool INIT>
-static cudaError_t launch_c(const kpm_graph *g, const StepParams &p, bool expl,
-                            bool first, cudaStream_t st) {
-  constexpr int U = (C == 4) ? 4 : 8;
+static cudaError_t launch_c(const kpm_run *r, const StepParams &p, bool expl, bool first,
+                            cudaStream_t st) {
+  constexpr int U = (C == 4) ? KPM_U4 : 8;
   const int threads = 256;
   size_t smem = (MODE == MODE_LDOS) ? 0 : (size_t)(threads / 32) * 2 * p.ld * sizeof(double);
   void (*kern)(StepParams);
@@ -303,17 +521,24 @@ static cudaError_t launch_c(const kpm_graph *g, const StepParams &p, bool expl,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<g->n_chunks, threads, smem, st>>>(p);
+  const int64_t items = p.n_chunks + (INIT ? 0 : p.n_heavy_tasks);
+  int64_t grid = (int64_t)r->g->ctx->sm_count * resident_blocks(kern, smem);
+  const int64_t need = (items + 7) / 8;  // 8 warps per CTA
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, threads, smem, st>>>(p);
   return cudaGetLastError();
 }
 
 template <int MODE, bool INIT>
-static cudaError_t launch_mode(const kpm_graph *g, int cpl, const StepParams &p,
-                               bool expl, bool first, cudaStream_t st) {
-  switch (cpl) {
-    case 1: return launch_c<1, MODE, INIT>(g, p, expl, first, st);
-    case 2: return launch_c<2, MODE, INIT>(g, p, expl, first, st);
-    default: return launch_c<4, MODE, INIT>(g, p, expl, first, st);
+static cudaError_t launch_mode(const kpm_run *r, const StepParams &p, bool expl, bool first,
+                               cudaStream_t st) {
+  switch (r->cpl) {
+    case 1: return launch_c<1, MODE, INIT>(r, p, expl, first, st);
+    case 2: return launch_c<2, MODE, INIT>(r, p, expl, first, st);
+    default: return launch_c<4, MODE, INIT>(r, p, expl, first, st);
   }
 }
 
@@ -323,14 +548,14 @@ static cudaError_t launch_step(const kpm_run *r, const StepParams &p, bool init,
   if (r->g->n_chunks == 0) return cudaSuccess;
   switch (r->mode) {
     case KPM_MODE_DOS_DOUBLING:
-      return init ? launch_mode<MODE_DBL, true>(r->g, r->cpl, p, expl, first, st)
-                  : launch_mode<MODE_DBL, false>(r->g, r->cpl, p, expl, first, st);
+      return init ? launch_mode<MODE_DBL, true>(r, p, expl, first, st)
+                  : launch_mode<MODE_DBL, false>(r, p, expl, first, st);
     case KPM_MODE_DOS_DIRECT:
-      return init ? launch_mode<MODE_DIRECT, true>(r->g, r->cpl, p, expl, first, st)
-                  : launch_mode<MODE_DIRECT, false>(r->g, r->cpl, p, expl, first, st);
+      return init ? launch_mode<MODE_DIRECT, true>(r, p, expl, first, st)
+                  : launch_mode<MODE_DIRECT, false>(r, p, expl, first, st);
     default:
-      return init ? launch_mode<MODE_LDOS, true>(r->g, r->cpl, p, expl, first, st)
-                  : launch_mode<MODE_LDOS, false>(r->g, r->cpl, p, expl, first, st);
+      return init ? launch_mode<MODE_LDOS, true>(r, p, expl, first, st)
+                  : launch_mode<MODE_LDOS, false>(r, p, expl, first, st);
   }
 }
 
@@ -350,19 +575,34 @@ static StepParams base_params(const kpm_run *r) {
   p.ldos_raw = (r->flags & KPM_LDOS_RAW) != 0;
   p.ld = r->ld;
   p.chunk_start = g->chunk_start;
+  p.n_chunks = g->n_chunks;
   p.partial = r->partial;
   p.flag = r->flag;
+  p.queue = r->queue;
+  p.heavy_rows = g->heavy_rows;
+  p.n_heavy = g->n_heavy;
+  p.heavy_threshold = g->heavy_threshold;
+  const int64_t nsl = (r->ld + kSlice - 1) / kSlice;
+  p.n_heavy_tasks = g->n_heavy * nsl;
+  p.hpart = r->hpart;
+  p.hldos = r->hldos;
   return p;
 }
 
 static cudaError_t launch_finalize(const kpm_run *r, int which, int m, cudaStream_t st) {
   const int nred = which == 2 ? 2 : 1;
-  const int64_t warps = nred * r->k;
-  const int threads = 256;
-  const int64_t blocks = (warps * 32 + threads - 1) / threads;
   if (r->g->n_chunks == 0) return cudaSuccess;
-  finalize_kernel<<<(unsigned)blocks, threads, 0, st>>>(r->partial, r->g->n_chunks, r->ld,
-                                                       r->k, which, m, r->m_max, r->contrib);
+  const int n_groups = (r->g->n_chunks + kGroup - 1) / kGroup;
+  const int64_t work = (int64_t)n_groups * nred * r->k;
+  int64_t b1 = (work + 255) / 256;
+  if (b1 > 148 * 16) b1 = 148 * 16;
+  reduce_groups_kernel<<<(unsigned)b1, 256, 0, st>>>(r->partial, r->g->n_chunks, r->ld, r->k,
+                                                      nred, r->gpart);
+  const int64_t warps = nred * r->k;
+  const int64_t blocks = (warps * 32 + 255) / 256;
+  const int nh = which == 0 ? 0 : r->g->n_heavy;
+  finalize_kernel<<<(unsigned)blocks, 256, 0, st>>>(r->gpart, n_groups, r->hpart, nh, r->ld,
+                                                     r->k, which, m, r->m_max, r->contrib);
   return cudaGetLastError();
 }
 
@@ -521,11 +761,17 @@ int kpm_run_create(kpm_graph *g, int64_t k, int32_t mode, int32_t m_max,
   if (m_max >= 1) A((void **)&r->b, blk);
   if (mode != KPM_MODE_DOS_DOUBLING) A((void **)&r->z, blk);
   A((void **)&r->flag, sizeof(int32_t) * 4);
+  A((void **)&r->queue, sizeof(unsigned long long));
+  const int64_t nh = g->n_heavy > 0 ? g->n_heavy : 1;
+  if (mode == KPM_MODE_LDOS) A((void **)&r->hldos, sizeof(double) * nh * ((r->ld + 15) / 16));
+  else A((void **)&r->hpart, sizeof(double) * nh * 2 * r->ld);
   if (mode == KPM_MODE_LDOS) {
     A((void **)&r->ldos, sizeof(double) * (size_t)(g->n > 0 ? g->n : 1) * (m_max + 1));
     A((void **)&r->den, sizeof(double) * (size_t)(g->n > 0 ? g->n : 1));
   } else {
     A((void **)&r->partial, sizeof(double) * (size_t)(g->n_chunks > 0 ? g->n_chunks : 1) * 2 * r->ld);
+    A((void **)&r->gpart,
+      sizeof(double) * (size_t)((g->n_chunks + 31) / 32 + 1) * 2 * r->ld);
     A((void **)&r->contrib, sizeof(double) * (size_t)(m_max + 1) * r->ld);
   }
   if (e != cudaSuccess) {
@@ -618,6 +864,12 @@ int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
     KPM_CUDA(launch_step(r, p, false, first, st));
     if (r->timing) KPM_CUDA(cudaEventRecord(r->ev[2 * r->ev_used++ + 1], st));
     const int m = r->k_index + 1;
+    if (r->mode == KPM_MODE_LDOS && r->g->n_heavy > 0) {
+      const int nsl = (int)((r->ld + kSlice - 1) / kSlice);
+      ldos_heavy_kernel<<<(r->g->n_heavy + 127) / 128, 128, 0, st>>>(
+          r->hldos, r->g->heavy_rows, r->g->n_heavy, nsl, r->ldos, r->m_max + 1, m, r->flag);
+      KPM_CUDA(cudaGetLastError());
+    }
     if (r->mode == KPM_MODE_DOS_DOUBLING) KPM_CUDA(launch_finalize(r, 2, m, st));
     else if (r->mode == KPM_MODE_DOS_DIRECT) KPM_CUDA(launch_finalize(r, 1, m, st));
     r->prev = r->cur;
@@ -689,6 +941,10 @@ void kpm_run_free(kpm_run *r) {
   cudaFree(r->ldos);
   cudaFree(r->den);
   cudaFree(r->flag);
+  cudaFree(r->hpart);
+  cudaFree(r->hldos);
+  cudaFree(r->gpart);
+  cudaFree(r->queue);
   for (cudaEvent_t e : r->ev) cudaEventDestroy(e);
   delete r;
 }

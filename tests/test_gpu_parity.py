@@ -318,3 +318,67 @@ def test_error_semantics(kpm_ctx):
     assert np.all(raw.values[1] == 0.0)
     m0 = kp.dos_moments(sop, probes, 0)
     assert m0.values.shape == (1,) and m0.values[0] == pytest.approx(1.0, abs=1e-14)
+
+
+# ------------------------------------------------------- hub (heavy) rows
+@pytest.mark.parametrize("name", GRAPH_CASES)
+@pytest.mark.parametrize("mode", [_lib.MODE_DOS_DIRECT, _lib.MODE_DOS_DOUBLING,
+                                  _lib.MODE_LDOS])
+def test_hub_path_bitexact(golden, kpm_ctx, monkeypatch, name, mode):
+    """Force the column-sliced hub path (degree >= 3) and re-check the T
+    blocks bit-for-bit and the moments against the reference."""
+    monkeypatch.setenv("KPM_HEAVY_DEGREE", "3")
+    g = _graph(golden, name)
+    z = golden[f"{name}/probes"]
+    dev = kp.DeviceGraph.from_csr(g.n, g.row_ptr, g.col_idx)
+    steps = sorted(int(k.split("/T")[1]) for k in golden if k.startswith(f"{name}/T"))
+    run = Run(dev, z.shape[1], mode, 2 * max(steps) + 2)
+    run.set_probe_block(z, z.shape[1])
+    done = 0
+    for s in steps:
+        run.advance(s - done)
+        done = s
+        ptr, ld, _ = run.block()
+        t = _d2h(ptr, (g.n, ld), kpm_ctx)[:, : z.shape[1]]
+        assert np.array_equal(t, golden[f"{name}/T{s}"]), (name, s)
+    run.free()
+    nz, seed, m_dos, m_pdos = golden[f"{name}/meta"].tolist()
+    op = kp.NormalizedAdjacencyOperator(dev)
+    sop = kp.rescale_operator(op, (-1.0, 1.0))
+    probes = kp.ProbeMatrix(g.n, nz, "rademacher", seed, columns=z)
+    if mode == _lib.MODE_LDOS:
+        pd = kp.pdos_moments(sop, probes, m_pdos)
+        assert np.max(np.abs(pd.values - golden[f"{name}/pdos_values"])) <= 1e-12
+    else:
+        mom = kp.dos_moments(sop, probes, m_dos, doubling=mode == _lib.MODE_DOS_DOUBLING)
+        assert _normwise(mom.values, golden[f"{name}/dos_values"]) <= 1e-9
+
+
+def test_hub_path_large_degree(oracle, kpm_ctx, monkeypatch):
+    """A real hub (star + ER background, max degree ~6000) with 128 probes:
+    hub rows take the sliced path at the default threshold; T_3 bit-exact."""
+    rng = np.random.default_rng(0)
+    n = 20000
+    hub_nb = rng.choice(np.arange(1, n), 6000, replace=False)
+    eu = rng.integers(0, n, 60000)
+    ev = rng.integers(0, n, 60000)
+    u = np.concatenate([np.zeros(6000, dtype=np.int64), eu])
+    v = np.concatenate([hub_nb, ev])
+    dev = kp.DeviceGraph.from_edges(n, u, v)
+    assert dev.max_degree >= 6000
+    rp, ci, dinv = dev.export()
+    ci = ci.astype(np.int64)
+    data = oracle.normadj_values(rp, ci, dinv)
+    z = oracle.make_probes(n, 128, "rademacher", seed=1)
+    run = Run(dev, 128, _lib.MODE_DOS_DIRECT, 6)
+    run.set_probe_block(z, 128)
+    run.advance(3)
+    ptr, ld, _ = run.block()
+    got = _d2h(ptr, (n, ld), kpm_ctx)[:, :128]
+    run.free()
+    assert np.array_equal(got, oracle.c_recurrence_block(rp, ci, data, z, 3, threads=8))
+    op = kp.rescale_operator(kp.NormalizedAdjacencyOperator(dev), (-1.0, 1.0))
+    c = kp.dos_contrib(op, kp.ProbeMatrix(n, 128, "rademacher", 1, columns=z), 20,
+                       doubling=False)
+    want = oracle.c_dos_contrib(rp, ci, data, z, 20, threads=8)
+    assert _normwise(c, want) <= 1e-12
