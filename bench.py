@@ -45,7 +45,9 @@ sys.path.insert(0, REPO)
 CONFIGS = {
     # name: (kind, params, probes, moments)
     "c1": ("er", dict(n=10_000, p=1e-3, seed=0), 20, 200),
+    "c2": ("ba", dict(n=1_000_000, m=5, seed=1), 64, 100),
     "c3": ("rmat", dict(scale=24, edge_factor=16, seed=2), 128, 500),
+    "c4": ("motif", dict(n_ba=2_000_000, m=4, seed=3), 64, 300),
     "c5": ("rmat", dict(scale=26, edge_factor=16, seed=4), 256, 1000),
     "rmat20": ("rmat", dict(scale=20, edge_factor=16, seed=2), 128, 500),
 }
@@ -157,8 +159,22 @@ def build_graph(cfg, ctx):
     kind, prm, _, _ = CONFIGS[cfg]
     if kind == "rmat":
         return kp.DeviceGraph.rmat(prm["scale"], prm["edge_factor"], prm["seed"], ctx=ctx)
-    g = kp.erdos_renyi(prm["n"], prm["p"], seed=prm["seed"])
+    g = host_graph(cfg)
     return kp.DeviceGraph.from_csr(g.n, g.row_ptr, g.col_idx, ctx=ctx)
+
+
+def host_graph(cfg):
+    """Host GraphCSR of an ER / BA / motif-heavy config (reference generators)."""
+    import paper_1905_09758_b200 as kp
+
+    kind, prm, _, _ = CONFIGS[cfg]
+    if kind == "er":
+        return kp.erdos_renyi(prm["n"], prm["p"], seed=prm["seed"])
+    if kind == "ba":
+        return kp.preferential_attachment(prm["n"], prm["m"], seed=prm["seed"])
+    if kind == "motif":
+        return kp.testkit.motif_heavy(prm["n_ba"], prm["m"], prm["seed"])
+    raise ValueError(cfg)
 
 
 # ----------------------------------------------------------------- ours

@@ -199,6 +199,21 @@ __global__ void chunk_bounds(const int64_t *__restrict__ prefix, int64_t n,
   start[c] = (int32_t)lo;
 }
 
+// per-chunk largest light-row cost (for the work-queue order)
+__global__ void chunk_maxdeg(const int64_t *__restrict__ row_ptr,
+                             const int32_t *__restrict__ start, int32_t n_chunks,
+                             int64_t heavy, int64_t *__restrict__ out) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_chunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    int64_t mx = 0;
+    for (int32_t i = start[c]; i < start[c + 1]; ++i) {
+      int64_t d = row_ptr[i + 1] - row_ptr[i];
+      if (d < heavy && d > mx) mx = d;
+    }
+    out[c] = mx;
+  }
+}
+
 __global__ void gather_degrees(const int64_t *__restrict__ row_ptr,
                                const int32_t *__restrict__ rows, int64_t k,
                                int64_t *__restrict__ deg) {
@@ -262,6 +277,25 @@ int finish_graph(kpm_graph *g) {
   chunk_bounds<<<(int)((nch + 1 + 255) / 256), 256, 0, st>>>(prefix, n, g->n_chunks, target,
                                                                g->chunk_start);
   KPM_CUDA(cudaGetLastError());
+  {
+    // queue order: chunks holding the longest rows first (ties by id), so a
+    // long row never starts late; partial slots stay indexed by chunk id
+    int64_t *dmx = nullptr;
+    KPM_CUDA(cudaMalloc(&dmx, sizeof(int64_t) * nch));
+    chunk_maxdeg<<<grid_for(nch), 256, 0, st>>>(g->row_ptr, g->chunk_start, g->n_chunks,
+                                                g->heavy_threshold, dmx);
+    std::vector<int64_t> mx(nch);
+    KPM_CUDA(cudaMemcpyAsync(mx.data(), dmx, sizeof(int64_t) * nch, cudaMemcpyDeviceToHost, st));
+    KPM_CUDA(cudaStreamSynchronize(st));
+    cudaFree(dmx);
+    std::vector<int32_t> order(nch);
+    for (int64_t c = 0; c < nch; ++c) order[c] = (int32_t)c;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return mx[a] > mx[b]; });
+    KPM_CUDA(cudaMalloc(&g->chunk_order, sizeof(int32_t) * nch));
+    KPM_CUDA(cudaMemcpy(g->chunk_order, order.data(), sizeof(int32_t) * nch,
+                        cudaMemcpyHostToDevice));
+  }
 
   // heavy rows, ordered by (degree desc, row asc): deterministic, graph-only
   g->n_heavy = 0;
@@ -570,6 +604,7 @@ void kpm_graph_free(kpm_graph *g) {
   cudaFree(g->values);
   cudaFree(g->chunk_start);
   cudaFree(g->heavy_rows);
+  cudaFree(g->chunk_order);
   delete g;
 }
 

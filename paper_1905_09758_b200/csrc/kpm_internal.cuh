@@ -74,6 +74,7 @@ struct kpm_graph {
   // load-balanced schedule (depends on the graph only, never on k)
   int32_t n_chunks = 0;
   int32_t *chunk_start = nullptr;  // n_chunks+1 row boundaries
+  int32_t *chunk_order = nullptr;  // work-queue order of the chunks
   // rows with degree >= heavy_threshold are split over column slices and
   // worked by dedicated warps (degree-desc order); chunks skip them
   int64_t heavy_threshold = 0;
@@ -82,7 +83,7 @@ struct kpm_graph {
 };
 
 // degree from which a row is a "heavy" (hub) row (graph-only constant)
-static constexpr int64_t kHeavyDegree = 4096;
+static constexpr int64_t kHeavyDegree = 65536;
 
 struct kpm_run {
   kpm_graph *g = nullptr;

@@ -49,6 +49,7 @@ struct StepParams {
   int ldos_raw;            // KPM_LDOS_RAW
   int64_t ld;
   const int32_t *chunk_start;
+  const int32_t *chunk_order;
   double *partial;         // n_chunks x 2 x ld
   int32_t *flag;
   // heavy (hub) rows: column-sliced tasks at the head of the work queue
@@ -120,17 +121,25 @@ __device__ __forceinline__ void heavy_task(const StepParams &p, int64_t t) {
       if constexpr (EXPL) hl = p.vals[base + lane];
       else hl = __dmul_rn(di, __ldg(p.dinv + jl));
     }
-    double v[4][4];
+    double v[4][4], hv[4];
+    int jw[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      const int q = w * 8 + nb;
-      const int j = __shfl_sync(0xffffffffu, jl, q);
-      const double hv = __shfl_sync(0xffffffffu, hl, q);
+      jw[w] = __shfl_sync(0xffffffffu, jl, w * 8 + nb);
+      hv[w] = __shfl_sync(0xffffffffu, hl, w * 8 + nb);
+    }
+    // all four waves' gathers in flight before any is consumed
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) v[w][c] = 0.0;
-      if (q < cnt && active) ld4_masked(p.X + (size_t)j * ld + c0, avail, vec, v[w]);
+      if (w * 8 + nb < cnt && active)
+        ld4_masked(p.X + (size_t)(uint32_t)jw[w] * (size_t)ld + c0, avail, vec, v[w]);
+    }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) v[w][c] = __dmul_rn(hv, v[w][c]);
+    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[w][c] = __dmul_rn(hv[w], v[w][c]);
     }
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
@@ -300,7 +309,8 @@ __device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, doub
               const int j = __shfl_sync(0xffffffffu, jl, (q + u) & 31);
 #pragma unroll
               for (int c = 0; c < C; ++c) v[u][c] = 0.0;
-              if (q + u < cnt && active) ld_vec<C>(p.X + (size_t)j * ld + c0, v[u]);
+              if (q + u < cnt && active)
+                ld_vec<C>(p.X + (size_t)(uint32_t)j * (uint32_t)ld + c0, v[u]);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -411,7 +421,8 @@ kpm_step_kernel(const StepParams p) {
         continue;
       }
     }
-    light_chunk<C, MODE, EXPL, FIRST, INIT, U>(p, (int)((int64_t)item - n_heavy_tasks), my);
+    light_chunk<C, MODE, EXPL, FIRST, INIT, U>(
+        p, p.chunk_order[(int64_t)item - n_heavy_tasks], my);
   }
 }
 
@@ -575,6 +586,7 @@ static StepParams base_params(const kpm_run *r) {
   p.ldos_raw = (r->flags & KPM_LDOS_RAW) != 0;
   p.ld = r->ld;
   p.chunk_start = g->chunk_start;
+  p.chunk_order = g->chunk_order;
   p.n_chunks = g->n_chunks;
   p.partial = r->partial;
   p.flag = r->flag;
