@@ -185,6 +185,13 @@ int kpm_ldos(kpm_graph *g, const double *z, int64_t k, int32_t m_max,
 int kpm_rmat_edges(kpm_ctx *ctx, int scale, uint64_t seed, uint32_t ta,
                    uint32_t tab, uint32_t tabc, int64_t e0, int64_t count,
                    int64_t *u, int64_t *v);
+/* Host-side (no GPU): the reference's preferential_attachment(n, m, seed)
+ * (testkit.py:175-198) draw-for-draw.  pcg = numpy PCG64 state of
+ * default_rng(seed): {state_hi, state_lo, inc_hi, inc_lo, has_uint32,
+ * uinteger}.  u/v receive the m(m+1)/2 + (n-m-1)m canonical edges in the
+ * reference's order. */
+int kpm_gen_preferential_attachment(int64_t n, int64_t m, const uint64_t *pcg,
+                                    int64_t *u, int64_t *v);
 /* Fused R-MAT -> graph: draws n_edges edges as above and feeds them straight
  * into the device loader (== kpm_rmat_edges + kpm_graph_from_edges with
  * keep_loops = 0, without materialising u/v). */

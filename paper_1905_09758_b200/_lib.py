@@ -84,6 +84,7 @@ SIGNATURES = {
     "kpm_rmat_edges": (_c_int, [_c_vp, _c_int, _c_u64, _c_u32, _c_u32, _c_u32, _c_i64, _c_i64,
                                 _c_vp, _c_vp]),
     "kpm_graph_rmat": (_c_int, [_c_vp, _c_int, _c_i64, _c_u64, _c_u32, _c_u32, _c_u32, _PP]),
+    "kpm_gen_preferential_attachment": (_c_int, [_c_i64, _c_i64, _c_vp, _c_vp, _c_vp]),
 }
 
 _lib = None

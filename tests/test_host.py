@@ -61,13 +61,22 @@ def test_er_generator_matches_reference(golden_meta):
         assert _sha(g.row_ptr) == want["row_ptr"] and _sha(g.col_idx) == want["col_idx"], key
 
 
-@pytest.mark.parametrize("key", ["ba_300_3_4", "ba_5000_5_1", "ba_20000_5_1"])
+@pytest.mark.parametrize("key", ["ba_300_3_4", "ba_5000_5_1", "ba_20000_5_1",
+                                 "ba_1000000_5_1", "ba_2000000_4_3"])
 def test_ba_generator_matches_reference(golden_meta, key):
+    """Native PCG64 replay (libkpm host code) reproduces the reference's BA
+    graphs bit-for-bit, including the full C2 and C4 sizes."""
     want = golden_meta["generators"][key]
     _, n, m, s = key.split("_")
     g = kp.preferential_attachment(int(n), int(m), seed=int(s))
     assert g.nnz == want["nnz"]
     assert _sha(g.row_ptr) == want["row_ptr"] and _sha(g.col_idx) == want["col_idx"]
+
+
+def test_ba_python_path_matches_reference(golden_meta):
+    want = golden_meta["generators"]["ba_5000_5_1"]
+    g = kp.preferential_attachment(5000, 5, seed=1, native=False)
+    assert _sha(g.col_idx) == want["col_idx"]
 
 
 def test_graph_cases_reproduced(golden):
