@@ -272,30 +272,19 @@ int finish_graph(kpm_graph *g) {
   if (target < 256) target = 256;
   int64_t nch = (total + target - 1) / target;
   if (nch < 1) nch = 1;
-  g->n_chunks = (int32_t)nch;
-  KPM_CUDA(cudaMalloc(&g->chunk_start, sizeof(int32_t) * (nch + 1)));
-  chunk_bounds<<<(int)((nch + 1 + 255) / 256), 256, 0, st>>>(prefix, n, g->n_chunks, target,
-                                                               g->chunk_start);
-  KPM_CUDA(cudaGetLastError());
+  std::vector<int32_t> bounds(nch + 1);
   {
-    // queue order: chunks holding the longest rows first (ties by id), so a
-    // long row never starts late; partial slots stay indexed by chunk id
-    int64_t *dmx = nullptr;
-    KPM_CUDA(cudaMalloc(&dmx, sizeof(int64_t) * nch));
-    chunk_maxdeg<<<grid_for(nch), 256, 0, st>>>(g->row_ptr, g->chunk_start, g->n_chunks,
-                                                g->heavy_threshold, dmx);
-    std::vector<int64_t> mx(nch);
-    KPM_CUDA(cudaMemcpyAsync(mx.data(), dmx, sizeof(int64_t) * nch, cudaMemcpyDeviceToHost, st));
+    int32_t *dcs = nullptr;
+    KPM_CUDA(cudaMalloc(&dcs, sizeof(int32_t) * (nch + 1)));
+    chunk_bounds<<<(int)((nch + 1 + 255) / 256), 256, 0, st>>>(prefix, n, (int32_t)nch, target,
+                                                                 dcs);
+    KPM_CUDA(cudaGetLastError());
+    KPM_CUDA(cudaMemcpyAsync(bounds.data(), dcs, sizeof(int32_t) * (nch + 1),
+                             cudaMemcpyDeviceToHost, st));
     KPM_CUDA(cudaStreamSynchronize(st));
-    cudaFree(dmx);
-    std::vector<int32_t> order(nch);
-    for (int64_t c = 0; c < nch; ++c) order[c] = (int32_t)c;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int32_t a, int32_t b) { return mx[a] > mx[b]; });
-    KPM_CUDA(cudaMalloc(&g->chunk_order, sizeof(int32_t) * nch));
-    KPM_CUDA(cudaMemcpy(g->chunk_order, order.data(), sizeof(int32_t) * nch,
-                        cudaMemcpyHostToDevice));
+    cudaFree(dcs);
   }
+  std::vector<int32_t> heavy_sorted;
 
   // heavy rows, ordered by (degree desc, row asc): deterministic, graph-only
   g->n_heavy = 0;
@@ -333,10 +322,44 @@ int finish_graph(kpm_graph *g) {
       KPM_CUDA(cudaMalloc(&g->heavy_rows, sizeof(int32_t) * nh));
       KPM_CUDA(cudaMemcpy(g->heavy_rows, sorted.data(), sizeof(int32_t) * nh,
                           cudaMemcpyHostToDevice));
+      heavy_sorted = sorted;
     }
     g->n_heavy = nh;
     cudaFree(sel);
     cudaFree(dnum);
+  }
+  // every hub row becomes a singleton chunk (skipped by the light stream),
+  // so a light chunk is a run of light rows whose nonzeros can be streamed
+  for (int32_t h : heavy_sorted) {
+    bounds.push_back(h);
+    bounds.push_back(h + 1);
+  }
+  std::sort(bounds.begin(), bounds.end());
+  bounds.erase(std::unique(bounds.begin(), bounds.end()), bounds.end());
+  nch = (int64_t)bounds.size() - 1;
+  g->n_chunks = (int32_t)nch;
+  KPM_CUDA(cudaMalloc(&g->chunk_start, sizeof(int32_t) * (nch + 1)));
+  KPM_CUDA(cudaMemcpy(g->chunk_start, bounds.data(), sizeof(int32_t) * (nch + 1),
+                      cudaMemcpyHostToDevice));
+  {
+    // queue order: chunks holding the longest rows first (ties by id), so a
+    // long row never starts late; partial slots stay indexed by chunk id
+    int64_t *dmx = nullptr;
+    KPM_CUDA(cudaMalloc(&dmx, sizeof(int64_t) * (nch > 0 ? nch : 1)));
+    if (nch > 0)
+      chunk_maxdeg<<<grid_for(nch), 256, 0, st>>>(g->row_ptr, g->chunk_start, g->n_chunks,
+                                                  g->heavy_threshold, dmx);
+    std::vector<int64_t> mx(nch);
+    KPM_CUDA(cudaMemcpyAsync(mx.data(), dmx, sizeof(int64_t) * nch, cudaMemcpyDeviceToHost, st));
+    KPM_CUDA(cudaStreamSynchronize(st));
+    cudaFree(dmx);
+    std::vector<int32_t> order(nch);
+    for (int64_t c = 0; c < nch; ++c) order[c] = (int32_t)c;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t x, int32_t y) { return mx[x] > mx[y]; });
+    KPM_CUDA(cudaMalloc(&g->chunk_order, sizeof(int32_t) * (nch > 0 ? nch : 1)));
+    KPM_CUDA(cudaMemcpy(g->chunk_order, order.data(), sizeof(int32_t) * nch,
+                        cudaMemcpyHostToDevice));
   }
   KPM_CUDA(cudaStreamSynchronize(st));
   cudaFree(prefix);

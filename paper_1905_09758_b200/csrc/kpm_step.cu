@@ -26,6 +26,8 @@
 // column tile, so every gathered neighbour row is one coalesced 8*ld-byte
 // read; neighbour ids / weights are loaded 32 at a time by the lanes and
 // broadcast with shuffles, and U gathers are kept in flight per warp.
+#include <cstdlib>
+
 #include "kpm_internal.cuh"
 
 namespace kpm {
@@ -59,6 +61,7 @@ struct StepParams {
   int64_t heavy_threshold;
   int32_t n_chunks;
   unsigned long long *queue;  // work-queue counter (zeroed before each launch)
+  int stream;              // stream light chunks (single tile) across rows
   double *hpart;           // n_heavy x 2 x ld (global modes)
   double *hldos;           // n_heavy x n_slices (LDOS)
 };
@@ -390,19 +393,238 @@ __device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, doub
   }
 }
 
+// Row epilogue shared by the streamed path: y = acc (+ explicit shift/scale),
+// T_{k+1} = 2y - T_{k-1}, store, and fold the moment products of this row.
+template <int C, int MODE, bool EXPL, bool FIRST>
+__device__ __forceinline__ void stream_finish_row(const StepParams &p, int row, bool active,
+                                                  int64_t c0, const double (&acc)[C],
+                                                  const double (&xo)[C], const double (&pv)[C],
+                                                  const double (&zv)[C], double *my) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ld = p.ld;
+  double lsum = 0.0;
+  if (active) {
+    double y[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) y[c] = acc[c];
+    if constexpr (EXPL) {
+      if (p.shift != 0.0) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) y[c] = __dsub_rn(y[c], __dmul_rn(p.shift, xo[c]));
+      }
+      if (p.scale != 1.0) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) y[c] = __ddiv_rn(y[c], p.scale);
+      }
+    }
+    if constexpr (!FIRST) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) y[c] = __dsub_rn(__dmul_rn(2.0, y[c]), pv[c]);
+    }
+    st_vec<C>(p.Y + (size_t)row * ld + c0, y);
+    if constexpr (MODE == MODE_DBL) {
+      double *s1 = my + c0, *s2 = my + ld + c0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        s1[c] = __dadd_rn(s1[c], __dmul_rn(y[c], xo[c]));
+        s2[c] = __dadd_rn(s2[c], __dmul_rn(y[c], y[c]));
+      }
+    } else if constexpr (MODE == MODE_DIRECT) {
+      double *s1 = my + c0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) s1[c] = __dadd_rn(s1[c], __dmul_rn(zv[c], y[c]));
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c) lsum = __dadd_rn(lsum, __dmul_rn(zv[c], y[c]));
+    }
+  }
+  if constexpr (MODE == MODE_LDOS) {
+    const double num = warp_sum_fixed(lsum);
+    if (lane == 0) {
+      if (!isfinite(num)) atomicOr(p.flag, 1);
+      p.ldos[(size_t)row * p.ldos_stride + p.ldos_col] = num;
+    }
+  }
+}
+
+#ifndef KPM_STREAM_LA
+#define KPM_STREAM_LA 0
+#endif
+// Light chunk as ONE stream of nonzeros (single column tile, ld <= 32*C):
+// neighbour ids / weights are fetched 32 at a time across row boundaries and
+// U gathers stay in flight continuously, so short rows no longer serialise on
+// their own load latencies; a row is finished the moment its last neighbour
+// is added (same per-row sequential order => still bit-exact).  The next
+// row's own operands (T_k, T_{k-1}, z) are prefetched one row ahead.  Hub rows
+// are singleton chunks and never appear here.
+template <int C, int MODE, bool EXPL, bool FIRST, int U>
+__device__ __forceinline__ void light_stream(const StepParams &p, int chunk, double *my) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ld = p.ld;
+  const int64_t c0 = (int64_t)lane * C;
+  const bool active = c0 < ld;
+  const int r0 = p.chunk_start[chunk], r1 = p.chunk_start[chunk + 1];
+  if constexpr (MODE != MODE_LDOS) {
+    for (int64_t e = lane; e < 2 * ld; e += 32) my[e] = 0.0;
+    __syncwarp();
+  }
+  // a singleton chunk holding a hub row: its hub tasks write the row
+  if (r1 - r0 == 1 && p.n_heavy > 0 &&
+      p.row_ptr[r1] - p.row_ptr[r0] >= p.heavy_threshold) {
+    if constexpr (MODE != MODE_LDOS) {
+      double *out = p.partial + (size_t)chunk * 2 * ld;
+      for (int64_t e = lane; e < 2 * ld; e += 32) out[e] = 0.0;
+    }
+    return;
+  }
+  // lane window over the chunk's rows: row_ptr[wb+lane] and dinv[wb+lane]
+  int wb = r0;
+  int64_t wrp = p.row_ptr[min(r0 + lane, r1)];
+  double wdi = 0.0;
+  if constexpr (!EXPL) wdi = (r0 + lane < r1) ? p.dinv[r0 + lane] : 0.0;
+  auto refill = [&](int base) {
+    wb = base;
+    wrp = p.row_ptr[min(base + lane, r1)];
+    if constexpr (!EXPL) wdi = (base + lane < r1) ? p.dinv[base + lane] : 0.0;
+  };
+  // row_ptr[r] for wb <= r <= wb+31 (r <= r1)
+  auto rp = [&](int r) { return __shfl_sync(0xffffffffu, wrp, r - wb); };
+
+  const int64_t K0 = __shfl_sync(0xffffffffu, wrp, 0);
+  const int64_t K1 = p.row_ptr[r1];
+  int row = r0;
+  if (row + 1 - wb > 31) refill(row);
+  int64_t rend = rp(row + 1);
+  double di = 0.0;
+  if constexpr (!EXPL) di = __shfl_sync(0xffffffffu, wdi, row - wb);
+  // own operands of the current row; with KPM_STREAM_LA also of row+1
+  double xo[C], pv[C], zv[C];
+#if KPM_STREAM_LA
+  double nxo[C], npv[C], nzv[C];
+#endif
+  auto own = [&](int r, double (&a)[C], double (&b)[C], double (&cz)[C]) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) a[c] = b[c] = cz[c] = 0.0;
+    if (r < r1 && active) {
+      const size_t off = (size_t)r * ld + c0;
+      if constexpr (EXPL || MODE == MODE_DBL) ld_vec<C>(p.X + off, a);
+      if constexpr (!FIRST) ld_vec_rw<C>(p.Xprev + off, b);
+      if constexpr (MODE != MODE_DBL) ld_vec<C>(p.Z + off, cz);
+    }
+  };
+  own(row, xo, pv, zv);
+#if KPM_STREAM_LA
+  own(row + 1, nxo, npv, nzv);
+#endif
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+
+  // finish every row whose nonzeros are exhausted at position kk
+  auto advance = [&](int64_t kk) {
+    while (row < r1 && kk == rend) {
+      stream_finish_row<C, MODE, EXPL, FIRST>(p, row, active, c0, acc, xo, pv, zv, my);
+      ++row;
+      if (row >= r1) break;
+      if (row + 1 - wb > 31) refill(row);
+      rend = rp(row + 1);
+      if constexpr (!EXPL) di = __shfl_sync(0xffffffffu, wdi, row - wb);
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = 0.0;
+#if KPM_STREAM_LA
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        xo[c] = nxo[c];
+        pv[c] = npv[c];
+        zv[c] = nzv[c];
+      }
+      own(row + 1, nxo, npv, nzv);
+#else
+      own(row, xo, pv, zv);
+#endif
+    }
+  };
+  advance(K0);  // leading empty rows
+
+  for (int64_t kb = K0; kb < K1; kb += 32) {
+    const int cnt = (int)min((int64_t)32, K1 - kb);
+    int jl = 0;
+    double wl = 0.0;  // dinv_j (implicit) or the stored value (explicit)
+    if (lane < cnt) {
+      jl = p.col[kb + lane];
+      if constexpr (EXPL) wl = p.vals[kb + lane];
+      else wl = __ldg(p.dinv + jl);
+    }
+    for (int q = 0; q < cnt; q += U) {
+      double v[U][C];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = __shfl_sync(0xffffffffu, jl, (q + u) & 31);
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[u][c] = 0.0;
+        if (q + u < cnt && active)
+          ld_vec<C>(p.X + (size_t)(uint32_t)j * (uint32_t)ld + c0, v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double w = __shfl_sync(0xffffffffu, wl, (q + u) & 31);
+        if (q + u < cnt) {
+          double h;
+          if constexpr (EXPL) h = w;
+          else h = __dmul_rn(di, w);  // (1*dinv_i)*dinv_j, operators.py:110
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[u][c]));
+          advance(kb + q + u + 1);
+        }
+      }
+    }
+  }
+  advance(K1);  // trailing empty rows
+  if constexpr (MODE != MODE_LDOS) {
+    __syncwarp();
+    const int nred = MODE == MODE_DBL ? 2 : 1;
+    double *out = p.partial + (size_t)chunk * 2 * ld;
+    for (int64_t e = lane; e < nred * ld; e += 32) out[e] = my[e];
+    __syncwarp();
+  }
+}
+
 // Persistent fused step kernel.  Work items: [0, n_heavy_tasks) hub-row
 // slices in degree-descending order, then the light row chunks.  Warps grab
 // items from one atomic counter (dynamic load balance, hubs first); every item
 // writes its own partial slot, so the reduction order is fixed by the graph
 // alone -- independent of the schedule, the launch shape and the probe count.
-#ifndef KPM_MIN_BLOCKS
-#define KPM_MIN_BLOCKS 3
+// Occupancy / memory-level-parallelism per lane layout (tuned on B200 with
+// tools/step_timer.py): resident 256-thread CTAs per SM and gathers in flight.
+#ifndef KPM_MINB4
+#define KPM_MINB4 3
+#endif
+#ifndef KPM_MINB2
+#define KPM_MINB2 4
+#endif
+#ifndef KPM_MINB1
+#define KPM_MINB1 4
 #endif
 #ifndef KPM_U4
-#define KPM_U4 4  // gathers in flight per lane-pair for the 4-column layout
+#define KPM_U4 4
 #endif
+#ifndef KPM_U2
+#define KPM_U2 4
+#endif
+#ifndef KPM_U1
+#define KPM_U1 8
+#endif
+#ifndef KPM_STREAM_MAXC
+#define KPM_STREAM_MAXC 2  // stream light chunks for the 1- and 2-column layouts
+#endif
+template <int C>
+struct Tune {
+  static constexpr int minb = C == 4 ? KPM_MINB4 : (C == 2 ? KPM_MINB2 : KPM_MINB1);
+  static constexpr int u = C == 4 ? KPM_U4 : (C == 2 ? KPM_U2 : KPM_U1);
+};
+
 template <int C, int MODE, bool EXPL, bool FIRST, bool INIT, int U>
-__global__ void __launch_bounds__(256, KPM_MIN_BLOCKS)
+__global__ void __launch_bounds__(256, Tune<C>::minb)
 kpm_step_kernel(const StepParams p) {
   extern __shared__ double sacc[];  // [W][2][ld] per-warp accumulators
   const int lane = threadIdx.x & 31;
@@ -421,8 +643,16 @@ kpm_step_kernel(const StepParams p) {
         continue;
       }
     }
-    light_chunk<C, MODE, EXPL, FIRST, INIT, U>(
-        p, p.chunk_order[(int64_t)item - n_heavy_tasks], my);
+    const int chunk = p.chunk_order[(int64_t)item - n_heavy_tasks];
+    if constexpr (!INIT) {
+      if constexpr (C <= KPM_STREAM_MAXC) {
+        if (p.stream && p.ld <= 32 * C) {
+          light_stream<C, MODE, EXPL, FIRST, U>(p, chunk, my);
+          continue;
+        }
+      }
+    }
+    light_chunk<C, MODE, EXPL, FIRST, INIT, U>(p, chunk, my);
   }
 }
 
@@ -518,7 +748,7 @@ static int resident_blocks(K kern, size_t smem) {
 template <int C, int MODE, bool INIT>
 static cudaError_t launch_c(const kpm_run *r, const StepParams &p, bool expl, bool first,
                             cudaStream_t st) {
-  constexpr int U = (C == 4) ? KPM_U4 : 8;
+  constexpr int U = Tune<C>::u;
   const int threads = 256;
   size_t smem = (MODE == MODE_LDOS) ? 0 : (size_t)(threads / 32) * 2 * p.ld * sizeof(double);
   void (*kern)(StepParams);
@@ -598,6 +828,8 @@ static StepParams base_params(const kpm_run *r) {
   p.n_heavy_tasks = g->n_heavy * nsl;
   p.hpart = r->hpart;
   p.hldos = r->hldos;
+  p.stream = 1;
+  if (const char *e = getenv("KPM_STREAM")) p.stream = atoi(e);
   return p;
 }
 
