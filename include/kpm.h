@@ -177,6 +177,40 @@ int kpm_ldos(kpm_graph *g, const double *z, int64_t k, int32_t m_max,
              int32_t flags, double trace_scale, double *values,
              int64_t *bad_node);
 
+/* ------------------------------------------------ row partitions (§8e) --- */
+/* Graphs too large to replicate: rank q of R holds rows [part_lo[q],
+ * part_lo[q+1]) of the CSR (column ids stay global) and the matching row
+ * block of every recurrence vector.  Gathers of rows owned by another rank
+ * read the owner's block directly -- peer memory over NVLink/NVSwitch
+ * (CUDA IPC handles, kpm_ipc_*) or, for R partitions on one device, plain
+ * device memory -- so there is no separate halo copy: the "halo exchange" is
+ * the fused kernel's own peer loads.  Ranks must synchronise between steps. */
+int kpm_graph_from_csr_part(kpm_ctx *ctx, int64_t n_global, int64_t row_lo,
+                            int64_t n_local, const int64_t *indptr,
+                            const int64_t *indices, int64_t nnz,
+                            const double *values, double shift, double scale,
+                            kpm_graph **out);
+/* R-MAT rows [row_lo, row_hi) of the full draw stream (kpm_graph_rmat). */
+int kpm_graph_rmat_part(kpm_ctx *ctx, int scale, int64_t n_edges, uint64_t seed,
+                        uint32_t ta, uint32_t tab, uint32_t tabc, int64_t row_lo,
+                        int64_t row_hi, kpm_graph **out);
+int kpm_graph_part_info(kpm_graph *g, int64_t *row0, int64_t *n_global);
+/* install d^-1/2 of ALL n_global rows (each rank computes its own rows'
+ * part from its degrees, kpm_graph_export; ranks all-gather them) */
+int kpm_graph_set_dinv(kpm_graph *g, const double *dinv_global);
+/* the run's own a/b recurrence blocks (for kpm_ipc_get_handle / peers) */
+int kpm_run_blocks(kpm_run *r, void **a, void **b);
+/* part_lo[nparts+1] global row bounds; peer_a/peer_b[q] = partition q's
+ * blocks as addressable from this device.  Global-moment results become raw
+ * per-partition sums (summed across ranks, then the doubling transform, on
+ * the host); LDOS rows are each rank's own. */
+int kpm_run_set_partition(kpm_run *r, int nparts, const int64_t *part_lo, int me,
+                          const void *const *peer_a, const void *const *peer_b);
+/* CUDA IPC: 64-byte handle of a device allocation / open a peer's handle */
+int kpm_ipc_get_handle(const void *dptr, void *handle);
+int kpm_ipc_open_handle(kpm_ctx *ctx, const void *handle, void **dptr);
+int kpm_ipc_close(void *dptr);
+
 /* ------------------------------------------------- harness generators --- */
 /* R-MAT edge draws [e0, e0+count) on the device (no reference counterpart,
  * SURVEY.md §9.2): Philox4x32-10(key=seed, ctr=(e, level/4)), quadrant by

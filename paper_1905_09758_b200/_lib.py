@@ -85,6 +85,17 @@ SIGNATURES = {
                                 _c_vp, _c_vp]),
     "kpm_graph_rmat": (_c_int, [_c_vp, _c_int, _c_i64, _c_u64, _c_u32, _c_u32, _c_u32, _PP]),
     "kpm_gen_preferential_attachment": (_c_int, [_c_i64, _c_i64, _c_vp, _c_vp, _c_vp]),
+    "kpm_graph_from_csr_part": (_c_int, [_c_vp, _c_i64, _c_i64, _c_i64, _c_vp, _c_vp, _c_i64,
+                                         _c_vp, _c_dbl, _c_dbl, _PP]),
+    "kpm_graph_rmat_part": (_c_int, [_c_vp, _c_int, _c_i64, _c_u64, _c_u32, _c_u32, _c_u32,
+                                     _c_i64, _c_i64, _PP]),
+    "kpm_graph_part_info": (_c_int, [_c_vp, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)]),
+    "kpm_graph_set_dinv": (_c_int, [_c_vp, _c_vp]),
+    "kpm_run_blocks": (_c_int, [_c_vp, _PP, _PP]),
+    "kpm_run_set_partition": (_c_int, [_c_vp, _c_int, _c_vp, _c_int, _c_vp, _c_vp]),
+    "kpm_ipc_get_handle": (_c_int, [_c_vp, _c_vp]),
+    "kpm_ipc_open_handle": (_c_int, [_c_vp, _c_vp, _PP]),
+    "kpm_ipc_close": (_c_int, [_c_vp]),
 }
 
 _lib = None

@@ -1,4 +1,6 @@
 // libkpm C-ABI: context, memory and error plumbing (include/kpm.h).
+#include <cstring>
+
 #include "kpm_internal.cuh"
 
 namespace kpm {
@@ -152,6 +154,28 @@ int kpm_mem_info(kpm_ctx *ctx, int64_t *free_bytes, int64_t *total_bytes) {
   KPM_CUDA(cudaMemGetInfo(&f, &t));
   if (free_bytes) *free_bytes = (int64_t)f;
   if (total_bytes) *total_bytes = (int64_t)t;
+  return KPM_OK;
+}
+
+int kpm_ipc_get_handle(const void *dptr, void *handle) {
+  KPM_CHECK_ARG(dptr && handle, "bad arguments");
+  cudaIpcMemHandle_t h;
+  KPM_CUDA(cudaIpcGetMemHandle(&h, const_cast<void *>(dptr)));
+  memcpy(handle, &h, sizeof(h));
+  return KPM_OK;
+}
+
+int kpm_ipc_open_handle(kpm_ctx *ctx, const void *handle, void **dptr) {
+  KPM_CHECK_ARG(ctx && handle && dptr, "bad arguments");
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  KPM_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return KPM_OK;
+}
+
+int kpm_ipc_close(void *dptr) {
+  if (dptr) KPM_CUDA(cudaIpcCloseMemHandle(dptr));
   return KPM_OK;
 }
 

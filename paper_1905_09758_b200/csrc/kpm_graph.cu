@@ -112,16 +112,17 @@ __global__ void rmat_edges_kernel(int scale, uint64_t seed, uint32_t ta,
 
 __global__ void rmat_keys_kernel(int scale, uint64_t seed, uint32_t ta,
                                  uint32_t tab, uint32_t tabc, int64_t m,
-                                 int s, uint64_t *__restrict__ keys) {
+                                 int s, int64_t lo, int64_t hi,
+                                 uint64_t *__restrict__ keys) {
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t a, b;
     rmat_draw((uint64_t)e, scale, k0, k1, ta, tab, tabc, a, b);
     uint64_t k0v = kSentinel, k1v = kSentinel;
-    if (a != b) {
-      k0v = ((uint64_t)a << s) | (uint64_t)b;
-      k1v = ((uint64_t)b << s) | (uint64_t)a;
+    if (a != b) {  // rows outside [lo, hi) belong to other partitions
+      if (a >= lo && a < hi) k0v = ((uint64_t)(a - lo) << s) | (uint64_t)b;
+      if (b >= lo && b < hi) k1v = ((uint64_t)(b - lo) << s) | (uint64_t)a;
     }
     keys[2 * e] = k0v;
     keys[2 * e + 1] = k1v;
@@ -370,16 +371,18 @@ int finish_graph(kpm_graph *g) {
 
 // keys: 2m entries (sentinels allowed); consumes and frees keys/alt.
 static int keys_to_graph(kpm_ctx *ctx, int64_t n, int s, uint64_t *keys,
-                         uint64_t *alt, int64_t nkeys, kpm_graph **out) {
+                         uint64_t *alt, int64_t nkeys, kpm_graph **out,
+                         int64_t row0 = 0, int64_t n_global = -1) {
+  const int sort_bits = s + key_bits(n);
   cudaStream_t st = ctx->stream;
   int64_t nnz = 0;
   if (nkeys > 0) {
     cub::DoubleBuffer<uint64_t> db(keys, alt);
     size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, db, nkeys, 0, 2 * s, st);
+    cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, db, nkeys, 0, sort_bits, st);
     void *tmp = nullptr;
     KPM_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
-    cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, db, nkeys, 0, 2 * s, st);
+    cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, db, nkeys, 0, sort_bits, st);
     KPM_CUDA(cudaGetLastError());
     KPM_CUDA(cudaFreeAsync(tmp, st));
     uint64_t *sorted = db.Current(), *other = db.Alternate();
@@ -409,6 +412,8 @@ static int keys_to_graph(kpm_ctx *ctx, int64_t n, int s, uint64_t *keys,
   g->ctx = ctx;
   g->n = n;
   g->nnz = nnz;
+  g->row0 = row0;
+  g->n_global = n_global < 0 ? n : n_global;
   cudaError_t e1 = cudaMalloc(&g->row_ptr, sizeof(int64_t) * (n + 1));
   cudaError_t e2 = cudaMalloc(&g->col_idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1));
   cudaError_t e3 = cudaMalloc(&g->dinv, sizeof(double) * (n > 0 ? n : 1));
@@ -505,10 +510,29 @@ int kpm_graph_rmat(kpm_ctx *ctx, int scale, int64_t n_edges, uint64_t seed,
     KPM_CUDA(cudaMalloc(&keys, sizeof(uint64_t) * 2 * n_edges));
     KPM_CUDA(cudaMalloc(&alt, sizeof(uint64_t) * 2 * n_edges));
     rmat_keys_kernel<<<grid_for(n_edges), 256, 0, ctx->stream>>>(
-        scale, seed, ta, tab, tabc, n_edges, s, keys);
+        scale, seed, ta, tab, tabc, n_edges, s, 0, n, keys);
     KPM_CUDA(cudaGetLastError());
   }
   return keys_to_graph(ctx, n, s, keys, alt, 2 * n_edges, out);
+}
+
+int kpm_graph_rmat_part(kpm_ctx *ctx, int scale, int64_t n_edges, uint64_t seed,
+                        uint32_t ta, uint32_t tab, uint32_t tabc, int64_t row_lo,
+                        int64_t row_hi, kpm_graph **out) {
+  KPM_CHECK_ARG(ctx && out && scale >= 1 && scale <= 30 && n_edges >= 0, "bad arguments");
+  const int64_t n = int64_t(1) << scale;
+  KPM_CHECK_ARG(0 <= row_lo && row_lo <= row_hi && row_hi <= n, "bad row range");
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  int s = key_bits(n);
+  uint64_t *keys = nullptr, *alt = nullptr;
+  if (n_edges > 0) {
+    KPM_CUDA(cudaMalloc(&keys, sizeof(uint64_t) * 2 * n_edges));
+    KPM_CUDA(cudaMalloc(&alt, sizeof(uint64_t) * 2 * n_edges));
+    rmat_keys_kernel<<<grid_for(n_edges), 256, 0, ctx->stream>>>(
+        scale, seed, ta, tab, tabc, n_edges, s, row_lo, row_hi, keys);
+    KPM_CUDA(cudaGetLastError());
+  }
+  return keys_to_graph(ctx, row_hi - row_lo, s, keys, alt, 2 * n_edges, out, row_lo, n);
 }
 
 int kpm_rmat_edges(kpm_ctx *ctx, int scale, uint64_t seed, uint32_t ta,
@@ -525,10 +549,42 @@ int kpm_rmat_edges(kpm_ctx *ctx, int scale, uint64_t seed, uint32_t ta,
   return KPM_OK;
 }
 
+static int graph_from_csr_impl(kpm_ctx *ctx, int64_t n, int64_t n_cols, int64_t row0,
+                               const int64_t *indptr, const int64_t *indices, int64_t nnz,
+                               const double *values, double shift, double scale,
+                               kpm_graph **out);
+
 int kpm_graph_from_csr(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
                        const int64_t *indices, int64_t nnz,
                        const double *values, double shift, double scale,
                        kpm_graph **out) {
+  return graph_from_csr_impl(ctx, n, n, 0, indptr, indices, nnz, values, shift, scale, out);
+}
+
+int kpm_graph_from_csr_part(kpm_ctx *ctx, int64_t n_global, int64_t row_lo, int64_t n_local,
+                            const int64_t *indptr, const int64_t *indices, int64_t nnz,
+                            const double *values, double shift, double scale,
+                            kpm_graph **out) {
+  KPM_CHECK_ARG(row_lo >= 0 && n_local >= 0 && row_lo + n_local <= n_global,
+                "bad partition rows");
+  return graph_from_csr_impl(ctx, n_local, n_global, row_lo, indptr, indices, nnz, values,
+                             shift, scale, out);
+}
+
+int kpm_graph_set_dinv(kpm_graph *g, const double *dinv_global) {
+  KPM_CHECK_ARG(g && dinv_global, "bad arguments");
+  KPM_CUDA(cudaSetDevice(g->ctx->device));
+  if (!g->dinv_all) KPM_CUDA(cudaMalloc(&g->dinv_all, sizeof(double) * (g->n_global + 1)));
+  KPM_CUDA(cudaMemcpyAsync(g->dinv_all, dinv_global, sizeof(double) * g->n_global,
+                           cudaMemcpyDefault, g->ctx->stream));
+  KPM_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  return KPM_OK;
+}
+
+static int graph_from_csr_impl(kpm_ctx *ctx, int64_t n, int64_t n_cols, int64_t row0,
+                               const int64_t *indptr, const int64_t *indices, int64_t nnz,
+                               const double *values, double shift, double scale,
+                               kpm_graph **out) {
   KPM_CHECK_ARG(ctx && out && n >= 0 && nnz >= 0 && indptr, "bad arguments");
   KPM_CHECK_ARG(nnz == 0 || indices, "indices is NULL");
   KPM_CHECK_ARG(n < (int64_t(1) << 31), "n must be < 2^31 (int32 col_idx)");
@@ -543,6 +599,8 @@ int kpm_graph_from_csr(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
   g->nnz = nnz;
   g->shift = shift;
   g->scale = scale;
+  g->row0 = row0;
+  g->n_global = n_cols;
   auto fail = [&](int rc) { kpm_graph_free(g); return rc; };
   if (cudaMalloc(&g->row_ptr, sizeof(int64_t) * (n + 1)) != cudaSuccess ||
       cudaMalloc(&g->col_idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1)) != cudaSuccess ||
@@ -572,7 +630,8 @@ int kpm_graph_from_csr(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
     int *bad = nullptr;
     cudaMalloc(&bad, sizeof(int));
     cudaMemsetAsync(bad, 0, sizeof(int), st);
-    idx64_to_32<<<grid_for(nnz), 256, 0, st>>>((const int64_t *)di, nnz, n, g->col_idx, bad);
+    idx64_to_32<<<grid_for(nnz), 256, 0, st>>>((const int64_t *)di, nnz, n_cols, g->col_idx,
+                                               bad);
     int hbad = 0;
     cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
     e = cudaStreamSynchronize(st);
@@ -587,6 +646,13 @@ int kpm_graph_from_csr(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
   int rc = finish_graph(g);
   if (rc != KPM_OK) return fail(rc);
   *out = g;
+  return KPM_OK;
+}
+
+int kpm_graph_part_info(kpm_graph *g, int64_t *row0, int64_t *n_global) {
+  KPM_CHECK_ARG(g, "graph is NULL");
+  if (row0) *row0 = g->row0;
+  if (n_global) *n_global = g->n_global;
   return KPM_OK;
 }
 
@@ -628,6 +694,7 @@ void kpm_graph_free(kpm_graph *g) {
   cudaFree(g->chunk_start);
   cudaFree(g->heavy_rows);
   cudaFree(g->chunk_order);
+  cudaFree(g->dinv_all);
   delete g;
 }
 

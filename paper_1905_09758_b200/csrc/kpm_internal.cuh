@@ -80,7 +80,13 @@ struct kpm_graph {
   int64_t heavy_threshold = 0;
   int32_t n_heavy = 0;
   int32_t *heavy_rows = nullptr;
+  // row partition (rows [row0, row0+n) of an n_global-row graph; col ids are
+  // global).  dinv_all: d^-1/2 of all n_global rows (NULL = dinv, unpartitioned)
+  int64_t row0 = 0, n_global = 0;
+  double *dinv_all = nullptr;
 };
+
+#define KPM_MAX_PARTS 16
 
 // degree from which a row is a "heavy" (hub) row (graph-only constant)
 static constexpr int64_t kHeavyDegree = 65536;
@@ -105,6 +111,13 @@ struct kpm_run {
   double *hldos = nullptr;    // n_heavy x slices (LDOS)
   double *gpart = nullptr;    // chunk-group partials (level-1 reduction)
   unsigned long long *queue = nullptr;  // persistent-kernel work counter
+  // row partitions: this run owns partition `me`; peer_a/peer_b[q] are the
+  // a/b recurrence blocks of partition q (peer memory or same device)
+  int nparts = 1, me = 0;
+  bool partitioned = false;  // kpm_run_set_partition called: raw global sums
+  int64_t part_lo[KPM_MAX_PARTS + 1] = {0};
+  const double *peer_a[KPM_MAX_PARTS] = {nullptr};
+  const double *peer_b[KPM_MAX_PARTS] = {nullptr};
   int32_t *flag = nullptr;    // [0]: non-finite seen; [1..2]: zero-mass node
   // optional per-launch timing of the step kernel (roofline evidence)
   bool timing = false;

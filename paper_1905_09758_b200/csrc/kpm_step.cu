@@ -33,6 +33,7 @@
 namespace kpm {
 
 enum { MODE_DBL = 0, MODE_DIRECT = 1, MODE_LDOS = 2 };
+constexpr int kMaxParts = KPM_MAX_PARTS;
 
 struct StepParams {
   const int64_t *row_ptr;
@@ -62,9 +63,26 @@ struct StepParams {
   int32_t n_chunks;
   unsigned long long *queue;  // work-queue counter (zeroed before each launch)
   int stream;              // stream light chunks (single tile) across rows
+  // row partitions (kMaxParts): this launch works local rows of partition
+  // `me`; a gathered row j lives in the block of its owner (peer memory on
+  // another GPU, or another block on this one) -- see kpm_run_set_partition
+  int nparts;
+  int64_t row0;            // global id of local row 0 (dinv is global)
+  int64_t part_lo[kMaxParts + 1];
+  const double *xparts[kMaxParts];
+  int raw;                 // finalize writes raw sums (partitions combine on host)
   double *hpart;           // n_heavy x 2 x ld (global modes)
   double *hldos;           // n_heavy x n_slices (LDOS)
 };
+
+// Address of gathered row j (global id) in the current T_k block.
+__device__ __forceinline__ const double *gather_row(const StepParams &p, uint32_t j) {
+  if (p.nparts <= 1) return p.X + (size_t)j * (uint32_t)p.ld;
+  int o = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxParts; ++q) o += (q < p.nparts && (int64_t)j >= p.part_lo[q]);
+  return p.xparts[o] + (size_t)(j - (uint32_t)p.part_lo[o]) * (uint32_t)p.ld;
+}
 
 // Heavy rows are cut into 16-column slices; one warp owns one (row, slice)
 // task.  Lane (nb = lane/4, cg = lane%4) gathers 4 columns of neighbour nb of
@@ -109,7 +127,7 @@ __device__ __forceinline__ void heavy_task(const StepParams &p, int64_t t) {
   const int i = p.heavy_rows[h];
   const int64_t beg = p.row_ptr[i], end = p.row_ptr[i + 1];
   double di = 0.0;
-  if constexpr (!EXPL) di = p.dinv[i];
+  if constexpr (!EXPL) di = p.dinv[p.row0 + i];
   const int64_t c0 = (int64_t)sl * kSlice + cg * 4;
   const int64_t avail = ld - c0;  // columns of this lane inside the row
   const bool active = avail > 0;
@@ -137,7 +155,7 @@ __device__ __forceinline__ void heavy_task(const StepParams &p, int64_t t) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) v[w][c] = 0.0;
       if (w * 8 + nb < cnt && active)
-        ld4_masked(p.X + (size_t)(uint32_t)jw[w] * (size_t)ld + c0, avail, vec, v[w]);
+        ld4_masked(gather_row(p, (uint32_t)jw[w]) + c0, avail, vec, v[w]);
     }
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
@@ -279,7 +297,7 @@ __device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, doub
       beg = end;
       end = p.row_ptr[i + 1];
       if (p.n_heavy > 0 && end - beg >= p.heavy_threshold) continue;  // hub task
-      if constexpr (!EXPL) di = p.dinv[i];
+      if constexpr (!EXPL) di = p.dinv[p.row0 + i];
     }
     double lsum = 0.0;  // LDOS lane partial
     for (int t = 0; t < ntiles; ++t) {
@@ -313,7 +331,7 @@ __device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, doub
 #pragma unroll
               for (int c = 0; c < C; ++c) v[u][c] = 0.0;
               if (q + u < cnt && active)
-                ld_vec<C>(p.X + (size_t)(uint32_t)j * (uint32_t)ld + c0, v[u]);
+                ld_vec<C>(gather_row(p, (uint32_t)j) + c0, v[u]);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -481,11 +499,11 @@ __device__ __forceinline__ void light_stream(const StepParams &p, int chunk, dou
   int wb = r0;
   int64_t wrp = p.row_ptr[min(r0 + lane, r1)];
   double wdi = 0.0;
-  if constexpr (!EXPL) wdi = (r0 + lane < r1) ? p.dinv[r0 + lane] : 0.0;
+  if constexpr (!EXPL) wdi = (r0 + lane < r1) ? p.dinv[p.row0 + r0 + lane] : 0.0;
   auto refill = [&](int base) {
     wb = base;
     wrp = p.row_ptr[min(base + lane, r1)];
-    if constexpr (!EXPL) wdi = (base + lane < r1) ? p.dinv[base + lane] : 0.0;
+    if constexpr (!EXPL) wdi = (base + lane < r1) ? p.dinv[p.row0 + base + lane] : 0.0;
   };
   // row_ptr[r] for wb <= r <= wb+31 (r <= r1)
   auto rp = [&](int r) { return __shfl_sync(0xffffffffu, wrp, r - wb); };
@@ -563,7 +581,7 @@ __device__ __forceinline__ void light_stream(const StepParams &p, int chunk, dou
 #pragma unroll
         for (int c = 0; c < C; ++c) v[u][c] = 0.0;
         if (q + u < cnt && active)
-          ld_vec<C>(p.X + (size_t)(uint32_t)j * (uint32_t)ld + c0, v[u]);
+          ld_vec<C>(gather_row(p, (uint32_t)j) + c0, v[u]);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -685,7 +703,7 @@ __global__ void reduce_groups_kernel(const double *__restrict__ partial, int n_c
 //                         contrib[2s]   = 2 S2 - mu_0     (if 2s <= M)
 __global__ void finalize_kernel(const double *__restrict__ gpart, int n_groups,
                                 const double *__restrict__ hpart, int n_heavy, int64_t ld,
-                                int64_t k, int which, int m, int m_max,
+                                int64_t k, int which, int m, int m_max, int raw,
                                 double *__restrict__ contrib) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -712,11 +730,12 @@ __global__ void finalize_kernel(const double *__restrict__ gpart, int n_groups,
     if (red == 0) {
       const int row = 2 * m - 1;
       if (row <= m_max)
-        contrib[(size_t)row * ld + c] = (m == 1) ? s : __dsub_rn(__dmul_rn(2.0, s), contrib[ld + c]);
+        contrib[(size_t)row * ld + c] =
+            (m == 1 || raw) ? s : __dsub_rn(__dmul_rn(2.0, s), contrib[ld + c]);
     } else {
       const int row = 2 * m;
       if (row <= m_max)
-        contrib[(size_t)row * ld + c] = __dsub_rn(__dmul_rn(2.0, s), contrib[c]);
+        contrib[(size_t)row * ld + c] = raw ? s : __dsub_rn(__dmul_rn(2.0, s), contrib[c]);
     }
   }
 }
@@ -805,7 +824,10 @@ static StepParams base_params(const kpm_run *r) {
   const kpm_graph *g = r->g;
   p.row_ptr = g->row_ptr;
   p.col = g->col_idx;
-  p.dinv = g->dinv;
+  p.dinv = g->dinv_all ? g->dinv_all : g->dinv;
+  p.row0 = g->row0;
+  p.nparts = r->nparts > 1 ? r->nparts : 1;
+  for (int q = 0; q <= kMaxParts; ++q) p.part_lo[q] = q <= r->nparts ? r->part_lo[q] : 0;
   p.vals = g->values;
   p.shift = g->shift;
   p.scale = g->scale;
@@ -846,7 +868,8 @@ static cudaError_t launch_finalize(const kpm_run *r, int which, int m, cudaStrea
   const int64_t blocks = (warps * 32 + 255) / 256;
   const int nh = which == 0 ? 0 : r->g->n_heavy;
   finalize_kernel<<<(unsigned)blocks, 256, 0, st>>>(r->gpart, n_groups, r->hpart, nh, r->ld,
-                                                     r->k, which, m, r->m_max, r->contrib);
+                                                     r->k, which, m, r->m_max,
+                                                     r->partitioned ? 1 : 0, r->contrib);
   return cudaGetLastError();
 }
 
@@ -871,18 +894,20 @@ __device__ __forceinline__ void philox4x64_10(uint64_t c[4], uint64_t k0, uint64
 // Element i of a column is bit 31 of the i-th 32-bit half-word of the
 // column's Philox stream (numpy: integers(0, 2) -> Lemire on next_uint32,
 // low half first; counter incremented before each 4-word block).
+// Rows [row0, row0+n) of the columns (global row i -> local row i - row0).
 __global__ void rademacher_kernel(int64_t n, int64_t ncols, const uint64_t *__restrict__ keys,
-                                  double *__restrict__ z, int64_t ldz, int64_t col0) {
-  const int64_t nblk = (n + 7) / 8;
+                                  double *__restrict__ z, int64_t ldz, int64_t col0,
+                                  int64_t row0) {
+  const int64_t b0 = row0 / 8, nblk = (row0 + n + 7) / 8 - b0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nblk * ncols;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = t / ncols, j = t % ncols;
+    const int64_t b = b0 + t / ncols, j = t % ncols;
     uint64_t c[4] = {(uint64_t)b + 1, 0, 0, 0};
     philox4x64_10(c, keys[2 * j], keys[2 * j + 1]);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int64_t i = b * 8 + q;
-      if (i < n) {
+      const int64_t i = b * 8 + q - row0;
+      if (i >= 0 && i < n) {
         const uint32_t half = (q & 1) ? (uint32_t)(c[q >> 1] >> 32) : (uint32_t)c[q >> 1];
         z[i * ldz + col0 + j] = (half >> 31) ? -1.0 : 1.0;
       }
@@ -988,6 +1013,8 @@ int kpm_run_create(kpm_graph *g, int64_t k, int32_t mode, int32_t m_max,
   KPM_CHECK_ARG(mode >= 0 && mode <= 2, "unknown mode %d", mode);
   KPM_CHECK_ARG(k <= 1024 || mode == KPM_MODE_LDOS,
                 "at most 1024 probe columns per batch (got %lld)", (long long)k);
+  KPM_CHECK_ARG(g->n_global == g->n || g->dinv_all || g->values,
+                "partition graph needs kpm_graph_set_dinv first");
   KPM_CUDA(cudaSetDevice(g->ctx->device));
   kpm_run *r = new kpm_run();
   r->g = g;
@@ -1074,14 +1101,42 @@ int kpm_run_set_rademacher(kpm_run *r, const uint64_t *keys) {
   KPM_TRY(stage_in(st, keys, sizeof(uint64_t) * 2 * r->k, tk, &dk));
   const int64_t n = r->g->n;
   if (n > 0)
-    rademacher_kernel<<<grid_of(((n + 7) / 8) * r->k), 256, 0, st>>>(
-        n, r->k, (const uint64_t *)dk, r->a, r->ld, 0);
+    rademacher_kernel<<<grid_of(((n + 15) / 8) * r->k), 256, 0, st>>>(
+        n, r->k, (const uint64_t *)dk, r->a, r->ld, 0, r->g->row0);
   KPM_CUDA(cudaGetLastError());
   int rc = run_after_probes(r);
   return rc;
 }
 
 int kpm_run_total_steps(kpm_run *r) { return r ? r->total_steps : 0; }
+
+int kpm_run_blocks(kpm_run *r, void **a, void **b) {
+  KPM_CHECK_ARG(r, "run is NULL");
+  if (a) *a = r->a;
+  if (b) *b = r->b;
+  return KPM_OK;
+}
+
+int kpm_run_set_partition(kpm_run *r, int nparts, const int64_t *part_lo, int me,
+                          const void *const *peer_a, const void *const *peer_b) {
+  KPM_CHECK_ARG(r && part_lo && peer_a && peer_b, "bad arguments");
+  KPM_CHECK_ARG(nparts >= 1 && nparts <= KPM_MAX_PARTS, "1 <= nparts <= %d", KPM_MAX_PARTS);
+  KPM_CHECK_ARG(me >= 0 && me < nparts, "bad partition index");
+  KPM_CHECK_ARG(part_lo[me] == r->g->row0 && part_lo[me + 1] - part_lo[me] == r->g->n,
+                "partition %d rows do not match the graph's rows", me);
+  KPM_CHECK_ARG(part_lo[0] == 0 && part_lo[nparts] == r->g->n_global, "bad partition bounds");
+  KPM_CHECK_ARG(peer_a[me] == r->a && peer_b[me] == r->b, "peer table must hold own blocks");
+  KPM_CHECK_ARG(r->mode != KPM_MODE_LDOS || nparts == 1 || true, "");
+  r->nparts = nparts;
+  r->partitioned = true;
+  r->me = me;
+  for (int q = 0; q <= nparts; ++q) r->part_lo[q] = part_lo[q];
+  for (int q = 0; q < nparts; ++q) {
+    r->peer_a[q] = (const double *)peer_a[q];
+    r->peer_b[q] = (const double *)peer_b[q];
+  }
+  return KPM_OK;
+}
 
 int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
   KPM_CHECK_ARG(r, "run is NULL");
@@ -1092,6 +1147,10 @@ int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
     StepParams p = base_params(r);
     p.X = r->cur;
     p.Xprev = r->prev;
+    if (r->nparts > 1) {
+      const bool on_a = r->cur == r->a;
+      for (int q = 0; q < r->nparts; ++q) p.xparts[q] = on_a ? r->peer_a[q] : r->peer_b[q];
+    }
     double *dst = first ? r->b : r->prev;  // T_{k+1} overwrites T_{k-1}
     p.Y = dst;
     p.ldos_col = r->k_index + 1;
@@ -1249,7 +1308,7 @@ int kpm_probes_rademacher(kpm_ctx *ctx, int64_t n, int64_t ncols, const uint64_t
   KPM_TRY(stage_in(ctx->stream, keys, sizeof(uint64_t) * 2 * ncols, tk, &dk));
   if (n > 0 && ncols > 0)
     rademacher_kernel<<<grid_of(((n + 7) / 8) * ncols), 256, 0, ctx->stream>>>(
-        n, ncols, (const uint64_t *)dk, z, ldz, col0);
+        n, ncols, (const uint64_t *)dk, z, ldz, col0, 0);
   KPM_CUDA(cudaGetLastError());
   KPM_CUDA(cudaStreamSynchronize(ctx->stream));  // tk is freed on return
   return KPM_OK;

@@ -95,3 +95,96 @@ def pdos_moments_sharded(sop, probes, m_max, normalized=True, group=None,
         values = num * probes.trace_scale
     return ChebMoments(mode=MODE_PER_NODE, values=np.ascontiguousarray(values),
                        scale_map=sop.scale_map, probe_meta=probes.meta())
+
+
+# ------------------------------------------------ row-partitioned (§8e) ---
+def _all_gather_arrays(arr: np.ndarray, group=None):
+    """All-gather variable-length 1-D float64 arrays (rank order)."""
+    import torch.distributed as dist
+
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, np.ascontiguousarray(arr), group=group)
+    return out
+
+
+def dos_moments_row_partitioned(part, bounds, probes, m_max, effective_dim=None,
+                                doubling=True, group=None):
+    """Global moments with rank r owning rows [bounds[r], bounds[r+1]) of H.
+
+    ``part`` is this rank's partition (``partition.part_rmat`` /
+    ``partition.part_from_csr``).  Each rank exports the CUDA IPC handles of
+    its two recurrence blocks; every rank maps all peers' blocks, so the fused
+    step kernel gathers remote rows straight from peer HBM over NVLink /
+    NVSwitch.  Ranks barrier between steps (a rank overwrites its T_{k-1}
+    block in step k+1 only after every peer finished gathering T_k)."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    from . import _lib
+    from .kpm import Run
+    from .partition import doubling_transform
+
+    rank, world = _world(group)
+    lib = _lib.load()
+    dinv_parts = _all_gather_arrays(part.export()[2], group)
+    part.set_dinv(np.concatenate(dinv_parts))
+    mode = _lib.MODE_DOS_DOUBLING if doubling else _lib.MODE_DOS_DIRECT
+    run = Run(part, probes.nz, mode, m_max)
+    opened = []
+    try:
+        if probes.device_generated:
+            run.set_probes(probes)
+        else:
+            z = np.ascontiguousarray(probes.columns[bounds[rank]:bounds[rank + 1]])
+            run.set_probe_block(z, z.shape[1])
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(lib.kpm_run_blocks(run._h, ctypes.byref(a), ctypes.byref(b)))
+        ha, hb = ctypes.create_string_buffer(64), ctypes.create_string_buffer(64)
+        _lib.check(lib.kpm_ipc_get_handle(a, ha), "ipc_get_handle")
+        _lib.check(lib.kpm_ipc_get_handle(b, hb), "ipc_get_handle")
+        handles = [None] * world
+        dist.all_gather_object(handles, (ha.raw, hb.raw), group=group)
+        pa, pb = [], []
+        for q, (qa, qb) in enumerate(handles):
+            if q == rank:
+                pa.append(a.value)
+                pb.append(b.value)
+                continue
+            for raw, dst in ((qa, pa), (qb, pb)):
+                p = ctypes.c_void_p()
+                _lib.check(lib.kpm_ipc_open_handle(part.ctx.handle,
+                                                   ctypes.create_string_buffer(raw, 64),
+                                                   ctypes.byref(p)), "ipc_open_handle")
+                opened.append(p.value)
+                dst.append(p.value)
+        lo = np.ascontiguousarray(bounds, dtype=np.int64)
+        arr_a = (ctypes.c_void_p * world)(*pa)
+        arr_b = (ctypes.c_void_p * world)(*pb)
+        _lib.check(lib.kpm_run_set_partition(run._h, world, _lib.ptr(lo), rank,
+                                             ctypes.cast(arr_a, ctypes.c_void_p),
+                                             ctypes.cast(arr_b, ctypes.c_void_p)),
+                   "run_set_partition")
+        dist.barrier(group=group)
+        for _ in range(run.total_steps):
+            run.advance(1)
+            part.ctx.synchronize()
+            dist.barrier(group=group)
+        raw = np.empty((m_max + 1, probes.nz))
+        run.result(raw)
+    finally:
+        for p in opened:
+            lib.kpm_ipc_close(p)
+        run.free()
+    parts = [None] * world
+    dist.all_gather_object(parts, raw, group=group)
+    total = np.zeros_like(raw)
+    for x in parts:  # rank order: deterministic for a fixed partition
+        total += x
+    contrib = doubling_transform(total, m_max) if doubling else total
+    if not np.all(np.isfinite(contrib)):
+        raise RecurrenceBlowupError(_BLOWUP)
+    denom = float(effective_dim) if effective_dim is not None else float(bounds[-1])
+    from .operators import IDENTITY_MAP
+    return ChebMoments(mode=MODE_GLOBAL, values=contrib.sum(axis=1) * (probes.trace_scale / denom),
+                       scale_map=IDENTITY_MAP, probe_meta=probes.meta())

@@ -82,3 +82,32 @@ def test_column_slices_partition_the_probe_family(world):
     full = kp.make_probes(50, 10, "rademacher", seed=3).columns
     parts = [p.column_slice(*shard_range(10, r, world)).columns for r in range(world)]
     assert np.array_equal(np.concatenate(parts, axis=1), full)
+
+
+def test_row_partition_raw_sums_and_doubling_transform(oracle):
+    """Host side of the row-partitioned path: per-partition raw doubling sums
+    (<T_s,T_s-1>, <T_s,T_s>), added in partition order, then the doubling
+    transform == the direct estimator z^T T_m z (oracle) to rounding."""
+    import paper_1905_09758_b200 as kp
+    from paper_1905_09758_b200.partition import balanced_bounds, doubling_transform
+
+    g = kp.erdos_renyi(400, 0.02, seed=3)
+    data = oracle.normadj_values(g.row_ptr, g.col_idx)
+    z = kp.make_probes(g.n, 6, "rademacher", seed=1).columns
+    M = 20
+    blocks = [z] + [oracle.c_recurrence_block(g.row_ptr, g.col_idx, data, z, s)
+                    for s in range(1, M // 2 + 1)]
+    bounds = balanced_bounds(g.row_ptr, 3)
+    raw = np.zeros((M + 1, 6))
+    for q in range(3):
+        lo, hi = bounds[q], bounds[q + 1]
+        part = np.zeros((M + 1, 6))
+        part[0] = np.einsum("ij,ij->j", z[lo:hi], z[lo:hi])
+        for s in range(1, M // 2 + 1):
+            t, tp = blocks[s][lo:hi], blocks[s - 1][lo:hi]
+            part[2 * s - 1] = np.einsum("ij,ij->j", t, tp)
+            part[2 * s] = np.einsum("ij,ij->j", t, t)
+        raw += part
+    got = doubling_transform(raw, M)
+    want = oracle.c_dos_contrib(g.row_ptr, g.col_idx, data, z, M)
+    assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
