@@ -465,6 +465,9 @@ __device__ __forceinline__ void stream_finish_row(const StepParams &p, int row, 
   }
 }
 
+#ifndef KPM_FAST_MINC
+#define KPM_FAST_MINC 1  // smallest column layout that uses the full-wave fast path
+#endif
 #ifndef KPM_STREAM_LA
 #define KPM_STREAM_LA 0
 #endif
@@ -481,6 +484,7 @@ __device__ __forceinline__ void light_stream(const StepParams &p, int chunk, dou
   const int64_t ld = p.ld;
   const int64_t c0 = (int64_t)lane * C;
   const bool active = c0 < ld;
+  const bool full_lanes = ld == 32 * C;  // every lane owns C real columns
   const int r0 = p.chunk_start[chunk], r1 = p.chunk_start[chunk + 1];
   if constexpr (MODE != MODE_LDOS) {
     for (int64_t e = lane; e < 2 * ld; e += 32) my[e] = 0.0;
@@ -575,6 +579,26 @@ __device__ __forceinline__ void light_stream(const StepParams &p, int chunk, dou
     }
     for (int q = 0; q < cnt; q += U) {
       double v[U][C];
+      if (C >= KPM_FAST_MINC && full_lanes && q + U <= cnt && kb + q + U <= rend) {
+        // fast path: a full wave inside the current row -- no predicates,
+        // no per-neighbour row-end checks
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = __shfl_sync(0xffffffffu, jl, q + u);
+          ld_vec<C>(gather_row(p, (uint32_t)j) + c0, v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double w = __shfl_sync(0xffffffffu, wl, q + u);
+          double h;
+          if constexpr (EXPL) h = w;
+          else h = __dmul_rn(di, w);
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[u][c]));
+        }
+        advance(kb + q + U);
+        continue;
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int j = __shfl_sync(0xffffffffu, jl, (q + u) & 31);
@@ -621,7 +645,7 @@ __device__ __forceinline__ void light_stream(const StepParams &p, int chunk, dou
 #define KPM_MINB2 4
 #endif
 #ifndef KPM_MINB1
-#define KPM_MINB1 4
+#define KPM_MINB1 3
 #endif
 #ifndef KPM_U4
 #define KPM_U4 4
@@ -630,7 +654,7 @@ __device__ __forceinline__ void light_stream(const StepParams &p, int chunk, dou
 #define KPM_U2 4
 #endif
 #ifndef KPM_U1
-#define KPM_U1 8
+#define KPM_U1 4
 #endif
 #ifndef KPM_STREAM_MAXC
 #define KPM_STREAM_MAXC 2  // stream light chunks for the 1- and 2-column layouts
