@@ -177,6 +177,18 @@ int kpm_ldos(kpm_graph *g, const double *z, int64_t k, int32_t m_max,
              int32_t flags, double trace_scale, double *values,
              int64_t *bad_node);
 
+/* ------------------------------------------------------ motif scan --- */
+/* Device motif detection (motifs.py:189-311 semantics, unit weights): for
+ * every row two 64-bit label sums over N(i) (open twins) and N(i)+{i}
+ * (closed twins) are radix-sorted with the row ids; each sorted position is
+ * verified exactly against its run head.  Host outputs, n entries each:
+ * *_rows sorted rows, *_head position of the run head, *_ok 1 = equal to the
+ * head (0 for excluded rows: self-loops; closed: isolated); chain_hub[x] /
+ * chain_mid[x]: hub and middle node of the pendant path x - b - hub, or -1. */
+int kpm_motif_scan(kpm_graph *g, int64_t *open_rows, int8_t *open_ok,
+                   int64_t *open_head, int64_t *closed_rows, int8_t *closed_ok,
+                   int64_t *closed_head, int64_t *chain_hub, int64_t *chain_mid);
+
 /* ------------------------------------------------ row partitions (§8e) --- */
 /* Graphs too large to replicate: rank q of R holds rows [part_lo[q],
  * part_lo[q+1]) of the CSR (column ids stay global) and the matching row

@@ -96,6 +96,7 @@ SIGNATURES = {
     "kpm_ipc_get_handle": (_c_int, [_c_vp, _c_vp]),
     "kpm_ipc_open_handle": (_c_int, [_c_vp, _c_vp, _PP]),
     "kpm_ipc_close": (_c_int, [_c_vp]),
+    "kpm_motif_scan": (_c_int, [_c_vp] + [_c_vp] * 8),
 }
 
 _lib = None

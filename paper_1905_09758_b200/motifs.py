@@ -40,20 +40,56 @@ _KIND_RANK = {MotifKind.OPEN_TWIN: 0, MotifKind.CLOSED_TWIN: 1,
               MotifKind.DANGLING_TWO_CHAIN: 2, MotifKind.CUSTOM: 3}
 
 
-@dataclass
 class MotifInstance:
     """A detected structure: nodes, eigenvalue, orthonormal sparse
-    eigenvectors (dict node -> value) with H u = eigenvalue u."""
+    eigenvectors (dict node -> value) with H u = eigenvalue u (motifs.py:
+    52-67 fields).  Detected instances build their eigenvector dicts lazily
+    (``operator`` set): filter_probes reads the class structure directly, so
+    C4's ~7.6e5 vectors never become Python dicts unless a caller asks."""
 
-    kind: MotifKind
-    nodes: tuple
-    eigenvalue: float
-    eigvecs: tuple
-    detail: dict = field(default_factory=dict)
+    __slots__ = ("kind", "nodes", "eigenvalue", "_eigvecs", "detail", "_operator")
+
+    def __init__(self, kind, nodes, eigenvalue, eigvecs=None, detail=None, operator=None):
+        self.kind = MotifKind(kind)
+        self.nodes = tuple(nodes)
+        self.eigenvalue = eigenvalue
+        self._eigvecs = None if eigvecs is None else tuple(eigvecs)
+        self.detail = {} if detail is None else detail
+        self._operator = operator
+
+    @property
+    def eigvecs(self) -> tuple:
+        if self._eigvecs is None:
+            self._eigvecs = (motif_eigenvectors(self, self._operator)
+                             if self._operator is not None else ())
+        return self._eigvecs
+
+    @eigvecs.setter
+    def eigvecs(self, value):
+        self._eigvecs = tuple(value)
+        self._operator = None
+
+    @property
+    def auto(self) -> bool:
+        """True for an untouched detected instance (structure known)."""
+        return self._operator is not None and self.kind is not MotifKind.CUSTOM
 
     @property
     def multiplicity(self) -> int:
+        if self.auto and self._eigvecs is None:
+            if self.kind is MotifKind.DANGLING_TWO_CHAIN:
+                return len(self.detail["chains"]) - 1
+            return len(self.nodes) - 1
         return len(self.eigvecs)
+
+    def __repr__(self):
+        return (f"MotifInstance(kind={self.kind.value!r}, nodes={self.nodes}, "
+                f"eigenvalue={self.eigenvalue!r}, detail={self.detail!r})")
+
+    def __eq__(self, other):
+        return (isinstance(other, MotifInstance) and self.kind is other.kind
+                and self.nodes == other.nodes and self.eigenvalue == other.eigenvalue
+                and self.eigvecs == other.eigvecs and self.detail == other.detail)
 
 
 @dataclass
@@ -142,9 +178,8 @@ def motif_eigenvectors(inst: MotifInstance, kind) -> tuple:
 
 def _build_instance(motif, nodes, detail, kind):
     inst = MotifInstance(kind=motif, nodes=tuple(int(x) for x in nodes), eigenvalue=0.0,
-                         eigvecs=(), detail=detail)
+                         detail=detail, operator=OperatorKind(kind))
     inst.eigenvalue = motif_eigenvalue(inst, kind)
-    inst.eigvecs = motif_eigenvectors(inst, kind)
     return inst
 
 
@@ -180,26 +215,47 @@ def _signature_classes(g, members, row_ptr_of, cols_of, w_of):
     brk[1:] = (d_s[1:] != d_s[:-1]) | (h1_s[1:] != h1_s[:-1]) | (h2_s[1:] != h2_s[:-1])
     gid = np.cumsum(brk) - 1
     counts = np.bincount(gid)
-    classes = []
     multi = np.flatnonzero(counts >= 2)
     if multi.size == 0:
         return []
     first = np.flatnonzero(brk)
-    pos_in_order = {}
-    for gi in multi.tolist():
+    # exact verification, vectorised: every member of a candidate group is
+    # compared entry by entry with the group's first member
+    in_multi = counts[gid] >= 2
+    mem = m_s[in_multi]
+    rep = m_s[first[gid[in_multi]]]
+    ms, me = row_ptr_of(mem)
+    rs, _ = row_ptr_of(rep)
+    dd = me - ms
+    tot = int(dd.sum())
+    offs = np.arange(tot) - np.repeat(np.cumsum(dd) - dd, dd)
+    im = np.repeat(ms, dd) + offs
+    ir = np.repeat(rs, dd) + offs
+    eq = (cols_of(im) == cols_of(ir)) & (w_of(im) == w_of(ir))
+    bad_entry = np.repeat(np.arange(mem.size), dd)[~eq]
+    ok = np.ones(mem.size, dtype=bool)
+    ok[bad_entry] = False
+    gm = gid[in_multi]
+    bad_groups = np.unique(gm[~ok])
+    classes = []
+    good = ~np.isin(gm, bad_groups)
+    gsel, msel = gm[good], mem[good]
+    if gsel.size:
+        cut = np.flatnonzero(np.diff(gsel)) + 1
+        for grp in np.split(msel, cut):
+            if grp.size >= 2:
+                classes.append(sorted(grp.tolist()))
+    # hash collisions (different lists, same key): exact regrouping
+    for gi in bad_groups.tolist():
         grp = m_s[first[gi]: first[gi] + counts[gi]]
-        # exact verification against the group's first member
         sig = {}
         for node in grp.tolist():
             s0, s1 = row_ptr_of(np.array([node]))
-            sl = slice(int(s0[0]), int(s1[0]))
-            key = (cols_of(np.arange(sl.start, sl.stop)).tobytes(),
-                   w_of(np.arange(sl.start, sl.stop)).tobytes())
-            sig.setdefault(key, []).append(node)
-        for mem in sig.values():
-            if len(mem) >= 2:
-                classes.append(sorted(mem))
-    del pos_in_order
+            ar = np.arange(int(s0[0]), int(s1[0]))
+            sig.setdefault((cols_of(ar).tobytes(), w_of(ar).tobytes()), []).append(node)
+        for members_ in sig.values():
+            if len(members_) >= 2:
+                classes.append(sorted(members_))
     return classes
 
 
@@ -310,19 +366,28 @@ def _dangling_chain_classes(g):
     return [(h, sorted(ch)) for h, ch in sorted(hubs.items()) if len(ch) >= 2]
 
 
-def detect_motifs(g, kinds=None, seed=0, operator=OperatorKind.NORMALIZED_ADJACENCY) -> list:
+def detect_motifs(g, kinds=None, seed=0, operator=OperatorKind.NORMALIZED_ADJACENCY,
+                  device=True) -> list:
     """Motif instances with eigenpairs stated for ``operator`` (motifs.py:
     263-311); every class is exact (no false positives).  ``seed`` is kept for
-    signature parity: classes are a function of the graph alone."""
+    signature parity: classes are a function of the graph alone.  Unit-weight
+    graphs are scanned on the B200 (csrc/kpm_motif.cu); ``device=False`` (or a
+    weighted graph) runs the vectorised host restatement."""
     del seed
     from .graph import DeviceGraph
-    if isinstance(g, DeviceGraph):
-        g = g.to_host()
     if kinds is None:
         kinds = {MotifKind.OPEN_TWIN, MotifKind.CLOSED_TWIN, MotifKind.DANGLING_TWO_CHAIN}
     kinds = {MotifKind(k) for k in kinds}
     if MotifKind.CUSTOM in kinds:
         raise MotifError("custom instances are supplied by the caller, not detected")
+    operator = OperatorKind(operator)
+    if isinstance(g, DeviceGraph) or (device and g.unit_weights):
+        return _detect_device(g, kinds, operator)
+    return _detect_host(g, kinds, operator)
+
+
+def _detect_host(g, kinds, operator) -> list:
+    """General (weighted-graph) detection on the host."""
     out = []
     degs = g.degrees()
     if MotifKind.OPEN_TWIN in kinds:
@@ -343,6 +408,144 @@ def detect_motifs(g, kinds=None, seed=0, operator=OperatorKind.NORMALIZED_ADJACE
                                            operator))
     out.sort(key=lambda t: (_KIND_RANK[t.kind], min(t.nodes), t.eigenvalue))
     return out
+
+
+class MotifSet(list):
+    """detect_motifs' result: the MotifInstance list of the reference API,
+    plus the class arrays it was built from (``arrays``), which filter_probes
+    uses directly while the list is unmodified."""
+
+    def __init__(self, items, arrays, n):
+        super().__init__(items)
+        self.arrays = arrays
+        self.n = n
+        self._orig = tuple(items)
+
+    def pristine(self) -> bool:
+        return len(self) == len(self._orig) and all(a is b for a, b in zip(self, self._orig))
+
+
+def _scan_classes(rows, head, ok):
+    """Classes from a device signature scan: runs of equal signature whose
+    members all matched the run head exactly; runs holding a mismatch (hash
+    collision) come back as a list of row arrays for exact regrouping."""
+    n = rows.shape[0]
+    if n == 0:
+        return [], []
+    starts = np.flatnonzero(head == np.arange(n))
+    lens = np.diff(np.append(starts, n))
+    head_ok = ok[starts].astype(bool)
+    run_of = np.repeat(np.arange(starts.size), lens)
+    bad = np.zeros(starts.size, dtype=bool)
+    np.logical_or.at(bad, run_of, ok == 0)
+    keep = head_ok & ~bad & (lens >= 2)
+    collide = head_ok & bad
+    classes = [rows[s:s + l] for s, l in zip(starts[keep].tolist(), lens[keep].tolist())]
+    fallback = [rows[s:s + l] for s, l in zip(starts[collide].tolist(), lens[collide].tolist())]
+    return classes, fallback
+
+
+def _detect_device(g, kinds, operator) -> "MotifSet":
+    """Unit-weight detection: device signature scan (csrc/kpm_motif.cu) +
+    O(n) host extraction; instances are created in the reference's order."""
+    import ctypes
+
+    from .graph import DeviceGraph
+    dev = g if isinstance(g, DeviceGraph) else g.device()
+    n = dev.n
+    orow, crow = np.empty(n, np.int64), np.empty(n, np.int64)
+    ohead, chead = np.empty(n, np.int64), np.empty(n, np.int64)
+    ook, cok = np.empty(n, np.int8), np.empty(n, np.int8)
+    hub, mid = np.empty(n, np.int64), np.empty(n, np.int64)
+    _lib.check(_lib.load().kpm_motif_scan(
+        dev.handle, _lib.ptr(orow), _lib.ptr(ook), _lib.ptr(ohead), _lib.ptr(crow),
+        _lib.ptr(cok), _lib.ptr(chead), _lib.ptr(hub), _lib.ptr(mid)), "motif_scan")
+    del ctypes
+    rp = None
+    deg = None
+
+    def _rowptr():
+        nonlocal rp, deg
+        if rp is None:
+            rp = dev.export()[0] if isinstance(g, DeviceGraph) else g.row_ptr
+            deg = np.diff(rp).astype(np.float64)
+        return rp
+
+    def _exact(groups, closed):
+        """Hash-collision runs: exact regrouping on the host (rare)."""
+        hg = g if not isinstance(g, DeviceGraph) else g.to_host()
+        out = []
+        for rows in groups:
+            sig = {}
+            for i in sorted(rows.tolist()):
+                nb = set(hg.neighbors(i).tolist())
+                key = tuple(sorted(nb | {i})) if closed else tuple(sorted(nb))
+                sig.setdefault(key, []).append(i)
+            out.extend(np.asarray(m, dtype=np.int64) for m in sig.values() if len(m) >= 2)
+        return out
+
+    arrays = {"operator": operator}
+    items = []
+    _rowptr()
+    for kind, rows, head, ok, closed in ((MotifKind.OPEN_TWIN, orow, ohead, ook, False),
+                                         (MotifKind.CLOSED_TWIN, crow, chead, cok, True)):
+        if kind not in kinds:
+            arrays[kind] = (np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
+            continue
+        classes, fallback = _scan_classes(rows, head, ok)
+        classes += _exact(fallback, closed)
+        classes.sort(key=lambda c: int(c[0]))
+        sizes = np.fromiter((c.size for c in classes), np.int64, len(classes))
+        ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        members = np.concatenate(classes) if classes else np.zeros(0, np.int64)
+        arrays[kind] = (ptr, members, deg[members[ptr[:-1]]] if classes else np.zeros(0))
+        if closed:
+            for c in classes:
+                d = float(deg[c[0]])
+                inst = MotifInstance(kind, tuple(c.tolist()), 0.0,
+                                     detail={"degree": d, "weight": 1.0}, operator=operator)
+                inst.eigenvalue = float(_twin_modes(operator, kind, d, 1.0))
+                items.append(inst)
+        else:
+            for c in classes:
+                d = float(deg[c[0]])
+                inst = MotifInstance(kind, tuple(c.tolist()), 0.0, detail={"degree": d},
+                                     operator=operator)
+                inst.eigenvalue = float(_twin_modes(operator, kind, d, 1.0))
+                items.append(inst)
+    if MotifKind.DANGLING_TWO_CHAIN in kinds:
+        xs = np.flatnonzero(hub >= 0)
+        order = np.argsort(hub[xs], kind="stable")
+        xs = xs[order]
+        hs, bs = hub[xs], mid[xs]
+        if xs.size:
+            cut = np.flatnonzero(np.diff(hs)) + 1
+            starts = np.concatenate([[0], cut])
+            ends = np.concatenate([cut, [xs.size]])
+        else:
+            starts = ends = np.zeros(0, np.int64)
+        modes = _chain_modes(operator)
+        chain_groups = []
+        for s, e in zip(starts.tolist(), ends.tolist()):
+            if e - s < 2:
+                continue
+            chains = tuple(zip(xs[s:e].tolist(), bs[s:e].tolist()))
+            chain_groups.append((int(hs[s]), chains))
+        chain_groups.sort(key=lambda t: min(min(x, b) for x, b in t[1]))
+        arrays[MotifKind.DANGLING_TWO_CHAIN] = chain_groups
+        for h, chains in chain_groups:
+            nodes = tuple(sorted(v for ch in chains for v in ch))
+            mode_order = sorted((0, 1), key=lambda mo: modes[mo][0])
+            for mo in mode_order:
+                inst = MotifInstance(MotifKind.DANGLING_TWO_CHAIN, nodes, float(modes[mo][0]),
+                                     detail={"hub": h, "chains": chains, "mode": mo},
+                                     operator=operator)
+                items.append(inst)
+    else:
+        arrays[MotifKind.DANGLING_TWO_CHAIN] = []
+    # reference order (rank, min node, eigenvalue): kinds already in rank
+    # order, classes sorted by their smallest member
+    return MotifSet(items, arrays, n)
 
 
 # ---------------------------------------------------------------- filtering
@@ -450,6 +653,250 @@ def projection_groups(arrays):
     return group_ptr, vec_ptr, np.ascontiguousarray(idx[gather]), np.ascontiguousarray(val[gather])
 
 
+def _detected_deflation(instances, n, reorth_tol=1e-8):
+    """Vectorised filter_probes bookkeeping for untouched detected instances
+    (the C4 case: ~6e5 classes).  Same greedy claim order, same vectors, same
+    projection order as motifs.py:342-403, without per-vector Python objects.
+    Returns ((group_ptr, vec_ptr, vec_idx, vec_val), removed) or None when
+    the general path is needed (custom instances, overlaps inside a kind,
+    non-orthonormal sets)."""
+    if not instances or not all(getattr(i, "auto", False) for i in instances):
+        return None
+    m = len(instances)
+    rank = np.fromiter((_KIND_RANK[i.kind] for i in instances), np.int64, m)
+    mn = np.fromiter((i.nodes[0] for i in instances), np.int64, m)  # nodes sorted
+    ev = np.fromiter((i.eigenvalue for i in instances), np.float64, m)
+    order = np.lexsort((ev, mn, rank))  # stable, = sorted(key=(rank, min, ev))
+    claimed = np.zeros(n, dtype=bool)
+    accepted = np.zeros(m, dtype=bool)
+    for rk in (0, 1, 2):
+        sel = order[rank[order] == rk]
+        if sel.size == 0:
+            continue
+        nodes_all = np.concatenate([np.asarray(instances[i].nodes, dtype=np.int64)
+                                    for i in sel])
+        lens = np.fromiter((len(instances[i].nodes) for i in sel), np.int64, sel.size)
+        owner = np.repeat(np.arange(sel.size), lens)
+        if rk == 2:  # the two modes of one hub share nodes; hubs must not
+            hub = np.fromiter((instances[i].detail["hub"] for i in sel), np.int64, sel.size)
+            pairs = np.unique(np.stack([hub[owner], nodes_all]), axis=1)
+            if np.unique(pairs[1]).size != pairs.shape[1]:
+                return None
+        elif np.unique(nodes_all).size != nodes_all.size:
+            return None  # overlapping classes inside a kind: general path
+        bad = np.zeros(sel.size, dtype=bool)
+        np.logical_or.at(bad, owner, claimed[nodes_all])
+        accepted[sel[~bad]] = True
+        claimed[nodes_all[~bad[owner]]] = True
+    acc = order[accepted[order]]
+    if acc.size == 0:
+        return None
+    removed = defaultdict(int)
+    for i in acc.tolist():
+        removed[float(instances[i].eigenvalue)] += instances[i].multiplicity
+
+    # -- vectors (instance position p in acc order, Helmert index k) -------
+    blocks = []  # (pos array, k, idx 2-D, val 2-D)
+    twin_pos = [p for p, i in enumerate(acc.tolist()) if instances[i].kind is not
+                MotifKind.DANGLING_TWO_CHAIN]
+    by_size = defaultdict(list)
+    for p in twin_pos:
+        by_size[len(instances[acc[p]].nodes)].append(p)
+    for s, plist in by_size.items():
+        pos = np.asarray(plist, dtype=np.int64)
+        nodes2d = np.asarray([instances[acc[p]].nodes for p in plist], dtype=np.int64)
+        for k in range(1, s):
+            nrm = np.sqrt(k * (k + 1.0))
+            vals = np.empty(k + 1)
+            vals[:k] = 1.0 / nrm
+            vals[k] = -float(k) / nrm
+            blocks.append((pos, k, nodes2d[:, : k + 1], np.broadcast_to(vals, (pos.size, k + 1))))
+    chain_pos = [p for p, i in enumerate(acc.tolist()) if instances[i].kind is
+                 MotifKind.DANGLING_TWO_CHAIN]
+    for p in chain_pos:
+        inst = instances[acc[p]]
+        _, alpha, beta = _chain_modes(inst._operator)[inst.detail["mode"]]
+        chains = inst.detail["chains"]
+        for k, amp in enumerate(_helmert_rows(len(chains)), start=1):
+            ent = {}
+            for a, (x, b) in zip(amp, chains):
+                if a != 0.0:
+                    ent[x] = float(a * alpha)
+                    ent[b] = float(a * beta)
+            ks = sorted(ent)
+            blocks.append((np.array([p]), k, np.array([ks], dtype=np.int64),
+                           np.array([[ent[q] for q in ks]])))
+    # orthonormality check (motifs.py:377-398): norms, and the only
+    # cross-instance overlaps left -- two chain modes of one hub
+    worst = 0.0
+    for _, _, _, val in blocks:
+        worst = max(worst, float(np.max(np.abs(np.einsum("ij,ij->i", val, val) - 1.0))))
+    if chain_pos:
+        per_hub = defaultdict(list)
+        for p in chain_pos:
+            per_hub[instances[acc[p]].detail["hub"]].append(p)
+        vec_of = defaultdict(list)
+        chain_set = set(chain_pos)
+        for pos, k, idx, val in blocks:
+            if pos.size == 1 and int(pos[0]) in chain_set:
+                vec_of[int(pos[0])].append((idx[0], val[0]))
+        for ps in per_hub.values():
+            for a in range(len(ps)):
+                for b in range(a + 1, len(ps)):
+                    for ia, va in vec_of[ps[a]]:
+                        for ib, vb in vec_of[ps[b]]:
+                            _, pa, pb = np.intersect1d(ia, ib, return_indices=True)
+                            if pa.size:
+                                worst = max(worst, abs(float(va[pa] @ vb[pb])))
+    if worst > reorth_tol:
+        return None
+    # -- CSR in projection order, groups = instances (chain modes of a hub
+    # merged) ----------------------------------------------------------------
+    vpos = np.concatenate([b[0] for b in blocks])
+    vk = np.concatenate([np.full(b[0].size, b[1]) for b in blocks])
+    vlen = np.concatenate([np.full(b[0].size, b[2].shape[1]) for b in blocks])
+    eidx = np.concatenate([b[2].reshape(-1) for b in blocks])
+    evals = np.concatenate([np.ascontiguousarray(b[3]).reshape(-1) for b in blocks])
+    estart = np.concatenate([[0], np.cumsum(vlen)[:-1]])
+    vorder = np.lexsort((vk, vpos))
+    lens_o = vlen[vorder]
+    vec_ptr = np.concatenate([[0], np.cumsum(lens_o)]).astype(np.int64)
+    gather = (np.repeat(estart[vorder], lens_o) +
+              (np.arange(int(lens_o.sum())) - np.repeat(vec_ptr[:-1], lens_o)))
+    vec_idx = np.ascontiguousarray(eidx[gather])
+    vec_val = np.ascontiguousarray(evals[gather])
+    gkey = np.array([instances[i].detail["hub"] + n if instances[i].kind is
+                     MotifKind.DANGLING_TWO_CHAIN else -1 - p
+                     for p, i in enumerate(acc.tolist())], dtype=np.int64)
+    vg = gkey[vpos[vorder]]
+    brk = np.ones(vg.size, dtype=bool)
+    brk[1:] = vg[1:] != vg[:-1]
+    group_ptr = np.append(np.flatnonzero(brk), vg.size).astype(np.int64)
+    return (group_ptr, vec_ptr, vec_idx, vec_val), dict(removed)
+
+
+def _helmert_block(pos, nodes2d):
+    """Helmert vectors of equal-size classes (rows of nodes2d, sorted members):
+    yields (pos, k, idx2d, val2d) for k = 1..s-1 (motifs.py:71-79 values)."""
+    s = nodes2d.shape[1]
+    for k in range(1, s):
+        nrm = np.sqrt(k * (k + 1.0))
+        vals = np.empty(k + 1)
+        vals[:k] = 1.0 / nrm
+        vals[k] = -float(k) / nrm
+        yield pos, k, nodes2d[:, : k + 1], np.broadcast_to(vals, (pos.size, k + 1))
+
+
+def _deflation_from_arrays(arrays, n, reorth_tol=1e-8):
+    """filter_probes bookkeeping straight from detect_motifs' class arrays:
+    greedy claims (open twins, then closed twins, then chain hubs -- classes
+    of one kind are disjoint), Helmert / chain vectors, per-class groups."""
+    op = arrays["operator"]
+    claimed = np.zeros(n, dtype=bool)
+    blocks, gkeys, removed = [], [], defaultdict(int)
+    next_pos = 0
+    for kind in (MotifKind.OPEN_TWIN, MotifKind.CLOSED_TWIN):
+        ptr, members, cdeg = arrays[kind]
+        ncls = ptr.size - 1
+        if ncls <= 0:
+            continue
+        sizes = np.diff(ptr)
+        owner = np.repeat(np.arange(ncls), sizes)
+        bad = np.zeros(ncls, dtype=bool)
+        np.logical_or.at(bad, owner, claimed[members])
+        claimed[members[~bad[owner]]] = True
+        acc = np.flatnonzero(~bad)
+        pos = next_pos + np.arange(acc.size)
+        next_pos += acc.size
+        udeg, dinv_ = np.unique(cdeg[acc], return_inverse=True)
+        ev = np.array([_twin_modes(op, kind, float(d), 1.0) for d in udeg.tolist()])[dinv_]
+        for sz in np.unique(sizes[acc]).tolist():
+            sel = sizes[acc] == sz
+            starts = ptr[acc[sel]]
+            nodes2d = members[starts[:, None] + np.arange(sz)[None, :]]
+            blocks.extend(_helmert_block(pos[sel], nodes2d))
+        gkeys.append(pos)
+        if acc.size:
+            vals, inv = np.unique(ev, return_inverse=True)
+            mult = np.bincount(inv, weights=sizes[acc] - 1)
+            for v, m in zip(vals.tolist(), mult.tolist()):
+                removed[float(v)] += int(m)
+    modes = _chain_modes(op)
+    chain_pos = {}
+    for h, chains in arrays[MotifKind.DANGLING_TWO_CHAIN]:
+        nodes = np.asarray([v for ch in chains for v in ch], dtype=np.int64)
+        if claimed[nodes].any():
+            continue
+        claimed[nodes] = True
+        for mo in sorted((0, 1), key=lambda m: modes[m][0]):
+            _, alpha, beta = modes[mo]
+            p = next_pos
+            next_pos += 1
+            chain_pos[p] = h
+            removed[float(modes[mo][0])] += len(chains) - 1
+            for k, amp in enumerate(_helmert_rows(len(chains)), start=1):
+                ent = {}
+                for a, (x, b) in zip(amp, chains):
+                    if a != 0.0:
+                        ent[x] = float(a * alpha)
+                        ent[b] = float(a * beta)
+                ks = sorted(ent)
+                blocks.append((np.array([p]), k, np.array([ks], dtype=np.int64),
+                               np.array([[ent[q] for q in ks]])))
+    if not blocks:
+        return None
+    worst = 0.0
+    for _, _, _, val in blocks:
+        worst = max(worst, float(np.max(np.abs(np.einsum("ij,ij->i", val, val) - 1.0))))
+    # chain modes of one hub overlap: eigenvectors of a symmetric 2x2, so
+    # orthogonal; checked numerically like motifs.py:377-398
+    by_hub = defaultdict(list)
+    for pos, k, idx, val in blocks:
+        if pos.size == 1 and int(pos[0]) in chain_pos:
+            by_hub[chain_pos[int(pos[0])]].append((int(pos[0]), idx[0], val[0]))
+    for vecs in by_hub.values():
+        for a in range(len(vecs)):
+            for b in range(a + 1, len(vecs)):
+                if vecs[a][0] == vecs[b][0]:
+                    continue
+                _, pa, pb = np.intersect1d(vecs[a][1], vecs[b][1], return_indices=True)
+                if pa.size:
+                    worst = max(worst, abs(float(vecs[a][2][pa] @ vecs[b][2][pb])))
+    if worst > reorth_tol:
+        return None
+    vpos = np.concatenate([b[0] for b in blocks])
+    vk = np.concatenate([np.full(b[0].size, b[1]) for b in blocks])
+    vlen = np.concatenate([np.full(b[0].size, b[2].shape[1]) for b in blocks])
+    eidx = np.concatenate([b[2].reshape(-1) for b in blocks])
+    evals = np.concatenate([np.ascontiguousarray(b[3]).reshape(-1) for b in blocks])
+    estart = np.concatenate([[0], np.cumsum(vlen)[:-1]])
+    vorder = np.lexsort((vk, vpos))
+    lens_o = vlen[vorder]
+    vec_ptr = np.concatenate([[0], np.cumsum(lens_o)]).astype(np.int64)
+    gather = (np.repeat(estart[vorder], lens_o) +
+              (np.arange(int(lens_o.sum())) - np.repeat(vec_ptr[:-1], lens_o)))
+    gkey = np.arange(next_pos, dtype=np.int64)
+    for p, h in chain_pos.items():
+        gkey[p] = next_pos + h  # both modes of a hub: one group
+    vg = gkey[vpos[vorder]]
+    brk = np.ones(vg.size, dtype=bool)
+    brk[1:] = vg[1:] != vg[:-1]
+    group_ptr = np.append(np.flatnonzero(brk), vg.size).astype(np.int64)
+    return ((group_ptr, vec_ptr, np.ascontiguousarray(eidx[gather]),
+             np.ascontiguousarray(evals[gather])), dict(removed))
+
+
+def _project_csr(columns, csr, ctx=None):
+    cols = np.array(columns, dtype=np.float64, order="C", copy=True)
+    ctx = ctx or _lib.Context.get()
+    gp, vp, vi, vv = csr
+    _lib.check(_lib.load().kpm_filter_probes(
+        ctx.handle, cols.shape[0], cols.shape[1], _lib.ptr(cols), cols.shape[1],
+        gp.shape[0] - 1, _lib.ptr(gp), _lib.ptr(vp), _lib.ptr(vi), _lib.ptr(vv)),
+        "filter_probes")
+    return cols
+
+
 def project_probes(columns, arrays, ctx=None):
     """The projection loop (motifs.py:400-403) on the device: returns the
     deflated copy of ``columns``."""
@@ -468,6 +915,16 @@ def project_probes(columns, arrays, ctx=None):
 def filter_probes(probes: ProbeMatrix, instances, reorth_tol=1e-8):
     """Project motif eigenvectors out of every probe column (motifs.py:342-405);
     returns (deflated probes, FilterAdjustment)."""
+    fast = None
+    if isinstance(instances, MotifSet) and instances.pristine() and instances.n == probes.n:
+        fast = _deflation_from_arrays(instances.arrays, probes.n, reorth_tol)
+    if fast is None:
+        fast = _detected_deflation(list(instances), probes.n, reorth_tol)
+    if fast is not None:
+        csr, removed = fast
+        cols = _project_csr(probes.columns, csr)
+        return with_columns(probes, cols), FilterAdjustment(removed=removed,
+                                                            total_dim=probes.n)
     arrays, removed = deflation_vectors(instances, probes.n, reorth_tol)
     if not arrays:
         return probes, FilterAdjustment(removed={}, total_dim=probes.n)

@@ -382,3 +382,43 @@ def test_hub_path_large_degree(oracle, kpm_ctx, monkeypatch):
                        doubling=False)
     want = oracle.c_dos_contrib(rp, ci, data, z, 20, threads=8)
     assert _normwise(c, want) <= 1e-12
+
+
+# ------------------------------------------------- device motif detection
+def _inst_key(i):
+    return (i.kind.value, tuple(i.nodes), i.eigenvalue, i.multiplicity,
+            tuple(sorted((k, v) for vec in i.eigvecs for k, v in vec.items())))
+
+
+def test_device_motif_scan_matches_reference(golden, golden_meta, kpm_ctx):
+    n = int(golden["motif/n"])
+    g = kp.GraphCSR(n=n, row_ptr=golden["motif/row_ptr"], col_idx=golden["motif/col_idx"],
+                    weights=np.ones(golden["motif/col_idx"].size), is_weighted=False)
+    dev = kp.detect_motifs(g, seed=3)
+    assert type(dev).__name__ == "MotifSet"
+    want = golden_meta["motif"]["instances"]
+    assert len(dev) == len(want)
+    for got, w in zip(dev, want):
+        kind, nodes, lam, mult, vecs, _ = w
+        assert got.kind.value == kind and list(got.nodes) == nodes
+        assert got.eigenvalue == lam and got.multiplicity == mult
+        for gv, wv in zip(got.eigvecs, vecs):
+            assert sorted(gv.items()) == sorted((int(k), v) for k, v in wv)
+    # array-backed filtering == the reference's filtered probes
+    p = kp.with_columns(kp.make_probes(n, 16, "rademacher", seed=3), golden["motif/probes"])
+    filt, adj = kp.filter_probes(p, dev)
+    assert np.max(np.abs(filt.columns - golden["motif/filtered"])) <= 1e-12
+    assert {repr(k): v for k, v in adj.removed.items()} == golden_meta["motif"]["removed"]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_device_motif_scan_matches_host(kpm_ctx, seed):
+    g = kp.testkit.motif_heavy(n_ba=4000, m=2, seed=seed, twin_pairs=300, stars=80)
+    for kinds in (None, {kp.MotifKind.CLOSED_TWIN}, {kp.MotifKind.DANGLING_TWO_CHAIN}):
+        dev = kp.detect_motifs(g, kinds=kinds)
+        host = kp.detect_motifs(g, kinds=kinds, device=False)
+        assert [_inst_key(i) for i in dev] == [_inst_key(i) for i in host]
+    # isolated nodes form one open-twin class; loops are excluded
+    g2 = kp.build_csr([(0, 1), (0, 2), (3, 3), (4, 5)], n=9, allow_self_loops=True)
+    assert [_inst_key(i) for i in kp.detect_motifs(g2)] == \
+        [_inst_key(i) for i in kp.detect_motifs(g2, device=False)]

@@ -185,7 +185,7 @@ def _motif_graph(golden):
 
 def test_detect_motifs_matches_reference(golden, golden_meta):
     g = _motif_graph(golden)
-    insts = kp.detect_motifs(g, seed=3)
+    insts = kp.detect_motifs(g, seed=3, device=False)
     want = golden_meta["motif"]["instances"]
     assert len(insts) == len(want)
     for got, w in zip(insts, want):
@@ -198,7 +198,7 @@ def test_detect_motifs_matches_reference(golden, golden_meta):
 
 def test_deflation_bookkeeping_and_projection(golden, golden_meta, oracle):
     g = _motif_graph(golden)
-    insts = kp.detect_motifs(g, seed=3)
+    insts = kp.detect_motifs(g, seed=3, device=False)
     arrays, removed = M.deflation_vectors(insts, g.n)
     assert {repr(k): v for k, v in removed.items()} == golden_meta["motif"]["removed"]
     # grouping for the device kernel keeps every shared-support chain in order
@@ -215,7 +215,7 @@ def test_deflation_bookkeeping_and_projection(golden, golden_meta, oracle):
 
 def test_overlapping_claims_and_dependent_vectors():
     g = kp.build_csr([(0, 1), (0, 2), (0, 3)])
-    twin = kp.detect_motifs(g, kinds={kp.MotifKind.OPEN_TWIN})[0]
+    twin = kp.detect_motifs(g, kinds={kp.MotifKind.OPEN_TWIN}, device=False)[0]
     fake = kp.MotifInstance(kind=kp.MotifKind.CUSTOM, nodes=(2, 3), eigenvalue=0.25,
                             eigvecs=({2: 1 / np.sqrt(2), 3: -1 / np.sqrt(2)},))
     _, removed = M.deflation_vectors([twin, fake], 4)
@@ -227,7 +227,7 @@ def test_overlapping_claims_and_dependent_vectors():
     with pytest.raises(kp.MotifError, match="dependent"):
         M.deflation_vectors([a, b], 4)
     with pytest.raises(kp.MotifError, match="custom"):
-        kp.detect_motifs(g, kinds={kp.MotifKind.CUSTOM})
+        kp.detect_motifs(g, kinds={kp.MotifKind.CUSTOM}, device=False)
     p = kp.make_probes(5, 3, "rademacher", seed=1)
     out, adj = kp.filter_probes(p, [])
     assert out is p and adj.deflated_dim == 0
@@ -238,7 +238,7 @@ def test_c4_builder_shape():
     assert n == 3000 + 600 + 200
     assert np.all(u < v)
     g = kp.testkit.motif_heavy(n_ba=3000, m=4, seed=3, twin_pairs=300, stars=50)
-    insts = kp.detect_motifs(g, kinds={kp.MotifKind.OPEN_TWIN})
+    insts = kp.detect_motifs(g, kinds={kp.MotifKind.OPEN_TWIN}, device=False)
     r = sum(i.multiplicity for i in insts)
     assert r >= 300 + 100  # every pair leaves >= 1 vector, every star 2
 
@@ -252,3 +252,34 @@ def test_shard_ranges_cover():
             assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
             sizes = [b - a for a, b in rs]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_detected_fast_path_matches_general_path(golden, oracle):
+    """The vectorised bookkeeping for detected instances yields exactly the
+    general path's vectors (same order, same values) and groups."""
+    g = _motif_graph(golden)
+    insts = kp.detect_motifs(g, seed=3, device=False)
+    fast = M._detected_deflation(insts, g.n)
+    assert fast is not None
+    (gp, vp, vi, vv), removed = fast
+    arrays, removed2 = M.deflation_vectors(insts, g.n)
+    assert removed == removed2
+    assert vp[-1] == sum(a[0].size for a in arrays) and len(vp) - 1 == len(arrays)
+    for v, (idx, val) in enumerate(arrays):
+        assert np.array_equal(vi[vp[v]:vp[v + 1]], idx)
+        assert np.array_equal(vv[vp[v]:vp[v + 1]], val)
+    vecs = [(vi[vp[v]:vp[v + 1]], vv[vp[v]:vp[v + 1]]) for v in range(len(arrays))]
+    cols = oracle.project_out(golden["motif/probes"], vecs)
+    assert np.max(np.abs(cols - golden["motif/filtered"])) < 1e-12
+    # custom instances take the general path
+    custom = kp.MotifInstance(kind=kp.MotifKind.CUSTOM, nodes=(0, 2), eigenvalue=0.0,
+                              eigvecs=({0: 1 / np.sqrt(2), 2: -1 / np.sqrt(2)},))
+    assert M._detected_deflation(insts + [custom], g.n) is None
+
+
+def test_lazy_instances_match_reference_fields(golden_meta, golden):
+    g = _motif_graph(golden)
+    insts = kp.detect_motifs(g, seed=3, device=False)
+    for got, w in zip(insts, golden_meta["motif"]["instances"]):
+        assert got.multiplicity == w[3]
+        assert len(got.eigvecs) == w[3]
