@@ -104,6 +104,10 @@ class Run:
             keys = probes.keys()
             _lib.check(_lib.load().kpm_run_set_rademacher(self._h, _lib.ptr(keys)),
                        "run_set_rademacher")
+        elif probes._columns is None and probes.device_block is not None:
+            blk = probes.device_block  # HBM-resident (e.g. motif-filtered): D2D
+            _lib.check(_lib.load().kpm_run_set_probes(self._h, blk.ptr, blk.ld),
+                       "run_set_probes")
         else:
             z = np.ascontiguousarray(probes.columns, dtype=np.float64)
             _lib.check(_lib.load().kpm_run_set_probes(self._h, _lib.ptr(z), z.shape[1]),

@@ -922,9 +922,22 @@ def filter_probes(probes: ProbeMatrix, instances, reorth_tol=1e-8):
         fast = _detected_deflation(list(instances), probes.n, reorth_tol)
     if fast is not None:
         csr, removed = fast
+        adj = FilterAdjustment(removed=removed, total_dim=probes.n)
+        if probes.device_generated:
+            # seeded Rademacher block: generate, deflate and keep it in HBM --
+            # the host block is only materialised if a caller reads .columns
+            from .probes import DeviceBlock
+            ctx = _lib.Context.get()
+            blk = DeviceBlock.rademacher(ctx, probes.n, probes.seed, probes.col_offset,
+                                         probes.nz)
+            gp, vp, vi, vv = csr
+            _lib.check(_lib.load().kpm_filter_probes(
+                ctx.handle, probes.n, probes.nz, blk.ptr, blk.ld, gp.shape[0] - 1,
+                _lib.ptr(gp), _lib.ptr(vp), _lib.ptr(vi), _lib.ptr(vv)), "filter_probes")
+            return ProbeMatrix(probes.n, probes.nz, probes.kind, probes.seed,
+                               col_offset=probes.col_offset, device_block=blk), adj
         cols = _project_csr(probes.columns, csr)
-        return with_columns(probes, cols), FilterAdjustment(removed=removed,
-                                                            total_dim=probes.n)
+        return with_columns(probes, cols), adj
     arrays, removed = deflation_vectors(instances, probes.n, reorth_tol)
     if not arrays:
         return probes, FilterAdjustment(removed={}, total_dim=probes.n)

@@ -77,26 +77,31 @@ class ProbeMatrix:
     is generated lazily (``device_generated`` is then True until materialised
     or replaced), letting the recurrence generate the block in HBM instead."""
 
-    def __init__(self, n, nz, kind, seed, columns=None, col_offset=0):
+    def __init__(self, n, nz, kind, seed, columns=None, col_offset=0, device_block=None):
         self.n = int(n)
         self.nz = int(nz)
         self.kind = ProbeKind(kind)
         self.seed = int(seed)
         self.col_offset = int(col_offset)  # first column index in the seeded family
         self._columns = None if columns is None else np.ascontiguousarray(columns)
+        self.device_block = device_block  # HBM-resident columns (e.g. filtered)
 
     @property
     def columns(self) -> np.ndarray:
         if self._columns is None:
-            self._columns = _host_columns(self.n, self.nz, self.kind, self.seed,
-                                          self.col_offset)
+            if self.device_block is not None:
+                self._columns = self.device_block.to_host()
+            else:
+                self._columns = _host_columns(self.n, self.nz, self.kind, self.seed,
+                                              self.col_offset)
         return self._columns
 
     @property
     def device_generated(self) -> bool:
         """True while the block is still the pristine seeded Rademacher block
         (the device regenerates it from philox_keys instead of uploading)."""
-        return self._columns is None and self.kind is ProbeKind.RADEMACHER
+        return (self._columns is None and self.device_block is None
+                and self.kind is ProbeKind.RADEMACHER)
 
     @property
     def deterministic(self) -> bool:
@@ -122,6 +127,10 @@ class ProbeMatrix:
         if self.device_generated:
             return ProbeMatrix(self.n, col1 - col0, self.kind, self.seed,
                                col_offset=self.col_offset + col0)
+        if self._columns is None and self.device_block is not None:
+            return ProbeMatrix(self.n, col1 - col0, self.kind, self.seed,
+                               col_offset=self.col_offset + col0,
+                               device_block=self.device_block.column_view(col0, col1))
         return ProbeMatrix(self.n, col1 - col0, self.kind, self.seed,
                            columns=np.ascontiguousarray(self.columns[:, col0:col1]),
                            col_offset=self.col_offset + col0)
@@ -129,6 +138,57 @@ class ProbeMatrix:
     def __repr__(self):
         return (f"ProbeMatrix(n={self.n}, nz={self.nz}, kind={self.kind.value}, "
                 f"seed={self.seed}, lazy={self._columns is None})")
+
+
+class DeviceBlock:
+    """An n x k fp64 probe block resident in HBM (row stride ld), owned by
+    libkpm's allocator; column views share the allocation."""
+
+    def __init__(self, ctx, n, k, ld=None, _base=None, _ptr=None):
+        import ctypes
+
+        from . import _lib
+        self.ctx, self.n, self.k = ctx, int(n), int(k)
+        self.ld = int(ld if ld is not None else k)
+        self._base = _base
+        if _ptr is None:
+            p = ctypes.c_void_p()
+            _lib.check(_lib.load().kpm_device_alloc(ctx.handle, 8 * max(self.n * self.ld, 1),
+                                                    ctypes.byref(p)), "device_alloc")
+            self.ptr, self._owner = p.value, True
+        else:
+            self.ptr, self._owner = _ptr, False
+
+    @classmethod
+    def rademacher(cls, ctx, n, seed, col0, ncols):
+        """Seeded Rademacher columns generated on the device (bit-identical
+        to make_probes)."""
+        from . import _lib
+        blk = cls(ctx, n, ncols)
+        keys = philox_keys(seed, col0 + ncols, col0, col0 + ncols)
+        _lib.check(_lib.load().kpm_probes_rademacher(ctx.handle, n, ncols, _lib.ptr(keys),
+                                                     blk.ptr, blk.ld, 0), "probes_rademacher")
+        return blk
+
+    def column_view(self, c0, c1):
+        return DeviceBlock(self.ctx, self.n, c1 - c0, self.ld, _base=self,
+                           _ptr=self.ptr + 8 * c0)
+
+    def to_host(self) -> np.ndarray:
+        from . import _lib
+        out = np.empty((self.n, self.ld))
+        _lib.check(_lib.load().kpm_memcpy(self.ctx.handle, _lib.ptr(out), self.ptr,
+                                          out.nbytes, 1), "memcpy")
+        self.ctx.synchronize()
+        return np.ascontiguousarray(out[:, : self.k])
+
+    def __del__(self):
+        try:
+            if self._owner and self.ptr:
+                from . import _lib
+                _lib.load().kpm_device_free(self.ctx.handle, self.ptr)
+        except Exception:
+            pass
 
 
 def make_probes(n, nz, kind=ProbeKind.RADEMACHER, seed=0) -> ProbeMatrix:

@@ -422,3 +422,24 @@ def test_device_motif_scan_matches_host(kpm_ctx, seed):
     g2 = kp.build_csr([(0, 1), (0, 2), (3, 3), (4, 5)], n=9, allow_self_loops=True)
     assert [_inst_key(i) for i in kp.detect_motifs(g2)] == \
         [_inst_key(i) for i in kp.detect_motifs(g2, device=False)]
+
+
+def test_filtered_probes_stay_on_device(golden, kpm_ctx):
+    """Seeded Rademacher probes are generated, deflated and consumed in HBM;
+    the result equals deflating the host block, and moments agree."""
+    n = int(golden["motif/n"])
+    g = kp.GraphCSR(n=n, row_ptr=golden["motif/row_ptr"], col_idx=golden["motif/col_idx"],
+                    weights=np.ones(golden["motif/col_idx"].size), is_weighted=False)
+    insts = kp.detect_motifs(g, seed=3)
+    lazy = kp.make_probes(n, 16, "rademacher", seed=3)
+    fd, adj = kp.filter_probes(lazy, insts)
+    assert fd.device_block is not None and fd._columns is None
+    fh, adj2 = kp.filter_probes(kp.with_columns(lazy, golden["motif/probes"]), insts)
+    assert adj.removed == adj2.removed
+    sop = kp.scaled_operator_for(g, "normalized-adjacency")
+    md = kp.dos_moments(sop, fd, 60, effective_dim=n - adj.deflated_dim)
+    mh = kp.dos_moments(sop, fh, 60, effective_dim=n - adj.deflated_dim)
+    assert np.array_equal(md.values, mh.values)
+    assert np.array_equal(fd.columns, fh.columns)
+    half = fd.column_slice(4, 12)
+    assert np.array_equal(half.columns, fh.columns[:, 4:12])
