@@ -240,8 +240,27 @@ __device__ __forceinline__ void ld_vec(const double *p, double (&v)[C]) {
 }
 
 // plain (coherent) load: Xprev may alias Y
+// T_{k-1} is read exactly once per step (its last use before being
+// overwritten) and T_{k+1} is only read back next step: with KPM_STREAM_HINTS
+// both move with evict-first ("streaming") cache hints so they do not push
+// the re-gathered hub rows of T_k out of L2.
+#ifndef KPM_STREAM_HINTS
+#define KPM_STREAM_HINTS 0
+#endif
 template <int C>
 __device__ __forceinline__ void ld_vec_rw(const double *p, double (&v)[C]) {
+#if KPM_STREAM_HINTS
+  if constexpr (C == 1) {
+    v[0] = __ldcs(p);
+  } else if constexpr (C == 2) {
+    double2 t = __ldcs(reinterpret_cast<const double2 *>(p));
+    v[0] = t.x; v[1] = t.y;
+  } else {
+    double2 t0 = __ldcs(reinterpret_cast<const double2 *>(p));
+    double2 t1 = __ldcs(reinterpret_cast<const double2 *>(p + 2));
+    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
+  }
+#else
   if constexpr (C == 1) {
     v[0] = *p;
   } else if constexpr (C == 2) {
@@ -252,10 +271,21 @@ __device__ __forceinline__ void ld_vec_rw(const double *p, double (&v)[C]) {
     double2 t1 = *reinterpret_cast<const double2 *>(p + 2);
     v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
   }
+#endif
 }
 
 template <int C>
 __device__ __forceinline__ void st_vec(double *p, const double (&v)[C]) {
+#if KPM_STREAM_HINTS
+  if constexpr (C == 1) {
+    __stcs(p, v[0]);
+  } else if constexpr (C == 2) {
+    __stcs(reinterpret_cast<double2 *>(p), make_double2(v[0], v[1]));
+  } else {
+    __stcs(reinterpret_cast<double2 *>(p), make_double2(v[0], v[1]));
+    __stcs(reinterpret_cast<double2 *>(p + 2), make_double2(v[2], v[3]));
+  }
+#else
   if constexpr (C == 1) {
     *p = v[0];
   } else if constexpr (C == 2) {
@@ -264,6 +294,7 @@ __device__ __forceinline__ void st_vec(double *p, const double (&v)[C]) {
     *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
     *reinterpret_cast<double2 *>(p + 2) = make_double2(v[2], v[3]);
   }
+#endif
 }
 
 __device__ __forceinline__ double warp_sum_fixed(double x) {
