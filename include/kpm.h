@@ -244,6 +244,35 @@ int kpm_gen_preferential_attachment(int64_t n, int64_t m, const uint64_t *pcg,
 int kpm_graph_rmat(kpm_ctx *ctx, int scale, int64_t n_edges, uint64_t seed,
                    uint32_t ta, uint32_t tab, uint32_t tabc, kpm_graph **out);
 
+/* --------------------------------------------- graph file ingest (§8f) --- */
+/* Replaces the line loops of _parse_edgelist / _parse_matrix_market
+ * (fileio.py:28-47, :76-95) and the id compaction of parse_graph_file
+ * (fileio.py:121-126).  The text (host or device pointer) is tokenised on the
+ * device, one thread per line: blank lines and lines starting with '%' (and
+ * '#' when KPM_PARSE_HASH_COMMENTS) are skipped; 2 or 3 whitespace-separated
+ * tokens; the first two are integers, stored minus `base`.
+ * Outputs are device arrays of n_lines entries (free with kpm_device_free):
+ * u, v and status (0 skipped, 2/3 token count, -1 malformed, -2 the host
+ * parser must decide: over-long or '_' integer tokens).  *unusual != 0 when
+ * the text holds bytes the device tokenizer does not model (non-ASCII,
+ * 0x1c-0x1f, NUL/DEL, bare '\r'); the caller then parses on the host. */
+#define KPM_PARSE_HASH_COMMENTS 1
+int kpm_parse_edges(kpm_ctx *ctx, const char *text, int64_t len, int64_t base,
+                    int flags, int64_t *n_lines, int64_t **u, int64_t **v,
+                    int8_t **status, int32_t *unusual);
+/* Compacts the kept lines (status 2/3) of kpm_parse_edges into m edges
+ * (device eu, ev; free with kpm_device_free).  compact_ids != 0: ids are
+ * mapped onto 0..n-1 by rank among the sorted unique ids, returned in
+ * *ids (device, n entries) -- np.unique + lookup, fileio.py:122-125;
+ * otherwise n = n_declared and *ids = NULL.  info[5]: [0] bit 0: some line
+ * had a weight token, bit 1: some line has status -2, [1] self-loop present, [2] a same-direction repeated edge
+ * (build_csr would sum weights), [3] first line (0-based) with status -1 or
+ * INT32_MAX, [4] an id outside [0, n). */
+int kpm_edges_finalize(kpm_ctx *ctx, int64_t n_lines, int64_t *u, int64_t *v,
+                       const int8_t *status, int compact_ids, int64_t n_declared,
+                       int64_t *m, int64_t *n, int64_t **eu, int64_t **ev,
+                       int64_t **ids, int32_t *info);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,7 @@ KPM_ENOMEM = -3
 KPM_ECUDA = -4
 KPM_EZEROMASS = -5
 KPM_ENODEV = -6
+KPM_PARSE_HASH_COMMENTS = 1
 
 MODE_DOS_DOUBLING = 0
 MODE_DOS_DIRECT = 1
@@ -97,6 +98,10 @@ SIGNATURES = {
     "kpm_ipc_open_handle": (_c_int, [_c_vp, _c_vp, _PP]),
     "kpm_ipc_close": (_c_int, [_c_vp]),
     "kpm_motif_scan": (_c_int, [_c_vp] + [_c_vp] * 8),
+    "kpm_parse_edges": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_int, _c_vp, _c_vp, _c_vp,
+                                 _c_vp, _c_vp]),
+    "kpm_edges_finalize": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_int, _c_i64,
+                                    _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp]),
 }
 
 _lib = None
