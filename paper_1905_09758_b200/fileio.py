@@ -7,7 +7,8 @@ symmetric (1-based, no compaction).  Same return value, same exceptions and
 messages (``FileFormatError`` with ``path:lineno``, ``GraphError`` from
 ``build_csr`` semantics).
 
-Design: the file is read once into pinned host memory and copied to HBM; the
+Design: the file is read by parallel positional reads into two pinned staging
+buffers whose H2D copies overlap the next read; the
 device numbers the lines, tokenises one line per thread, compacts the edge
 lines, ranks the ids (sort + unique + binary search) and feeds the edges to
 the device CSR loader (kpm_graph_from_edges, bit-identical to
@@ -26,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import time
 
 import numpy as np
 
@@ -39,6 +41,8 @@ _INT32_MAX = 0x7FFFFFFF
 
 #: "device" or "host": which path the last parse took (tests / diagnostics)
 last_ingest_path = None
+#: stage wall times of the last device parse (seconds; tools/ingest_bench.py)
+last_ingest_timing: dict = {}
 
 
 # ------------------------------------------------------------ host restatement
@@ -185,21 +189,82 @@ def _d2h(ctx, dptr, count, dtype):
     return out
 
 
-def _read_pinned(path, offset):
-    """File bytes [offset, EOF) in pinned host memory (one H2D copy later)."""
-    size = os.path.getsize(path) - offset
+_STAGE_BYTES = 1 << 27          # 128 MiB per pinned staging buffer
+_READ_THREADS = min(8, os.cpu_count() or 1)
+_staging = {}
+
+
+def _pinned_pair(ctx):
+    """Two pinned staging buffers per context, allocated once."""
+    bufs = _staging.get(ctx.handle)
+    if bufs is None:
+        lib = _lib.load()
+        bufs = []
+        for _ in range(2):
+            p = ctypes.c_void_p()
+            _lib.check(lib.kpm_host_alloc(_STAGE_BYTES, ctypes.byref(p)), "host_alloc")
+            bufs.append(p.value)
+        _staging[ctx.handle] = bufs
+    return bufs
+
+
+def _read_into(path, offset, addr, nbytes, pool):
+    """Parallel positional reads of [offset, offset+nbytes) into host memory
+    at addr (page-cache copies release the GIL and scale with threads)."""
+    piece = -(-nbytes // _READ_THREADS)
+
+    def one(k):
+        lo = k * piece
+        hi = min(nbytes, lo + piece)
+        if hi <= lo:
+            return 0
+        view = memoryview((ctypes.c_char * (hi - lo)).from_address(addr + lo)).cast("B")
+        with open(path, "rb", buffering=0) as fb:
+            fb.seek(offset + lo)
+            got = 0
+            while got < hi - lo:
+                r = fb.readinto(view[got:])
+                if not r:
+                    break
+                got += r
+        return got
+
+    got = sum(pool.map(one, range(_READ_THREADS)))
+    if got != nbytes:
+        raise OSError(f"{path}: short read ({got} of {nbytes} bytes)")
+
+
+def _upload_file(path, offset, ctx):
+    """File bytes [offset, EOF) copied to HBM: parallel reads into two pinned
+    staging buffers, each H2D copy overlapping the read of the next chunk.
+    Returns (device pointer owned by the caller, size)."""
+    from concurrent.futures import ThreadPoolExecutor
+    size = max(os.path.getsize(path) - offset, 0)
+    if size == 0:
+        return None, 0
     lib = _lib.load()
-    p = ctypes.c_void_p()
-    if size > 0:
-        _lib.check(lib.kpm_host_alloc(size, ctypes.byref(p)), "host_alloc")
-        buf = (ctypes.c_char * size).from_address(p.value)
-        with open(path, "rb") as fb:
-            fb.seek(offset)
-            got = fb.readinto(memoryview(buf).cast("B"))
-        if got != size:
-            lib.kpm_host_free(p)
-            raise OSError(f"{path}: short read ({got} of {size} bytes)")
-    return p.value, max(size, 0)
+    d = ctypes.c_void_p()
+    _lib.check(lib.kpm_device_alloc(ctx.handle, size, ctypes.byref(d)), "device_alloc")
+    try:
+        stage = _pinned_pair(ctx)
+        with ThreadPoolExecutor(_READ_THREADS) as pool:
+            pos, k = 0, 0
+            while pos < size:
+                nb = min(_STAGE_BYTES, size - pos)
+                buf = stage[k & 1]
+                # buf's previous copy (chunk k-2) was waited for last round;
+                # this read overlaps the copy of chunk k-1 from the other buffer
+                _read_into(path, offset + pos, buf, nb, pool)
+                ctx.synchronize()
+                _lib.check(lib.kpm_memcpy(ctx.handle, ctypes.c_void_p(d.value + pos),
+                                          ctypes.c_void_p(buf), nb, 0), "memcpy")
+                pos += nb
+                k += 1
+        ctx.synchronize()
+    except BaseException:
+        lib.kpm_device_free(ctx.handle, d)
+        raise
+    return d.value, size
 
 
 def _line_text(path, lineno):
@@ -223,24 +288,30 @@ def _device_ingest(path, mm, allow_self_loops, ctx):
         base, flags = 1, 0
     else:
         header_lines, offset, base, flags = 0, 0, 0, _lib.KPM_PARSE_HASH_COMMENTS
-    hptr, size = _read_pinned(path, offset)
+    t0 = time.perf_counter()
+    dtext, size = _upload_file(path, offset, ctx)
+    t1 = time.perf_counter()
+    last_ingest_timing.clear()
+    last_ingest_timing.update(bytes=size, upload_s=t1 - t0)
     with _DevArrays(ctx) as bufs:
         nl = ctypes.c_int64()
         du, dv, ds = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
         unusual = ctypes.c_int32()
         try:
-            rc = lib.kpm_parse_edges(ctx.handle, ctypes.c_void_p(hptr), size, base, flags,
+            rc = lib.kpm_parse_edges(ctx.handle, ctypes.c_void_p(dtext), size, base, flags,
                                      ctypes.byref(nl), ctypes.byref(du), ctypes.byref(dv),
                                      ctypes.byref(ds), ctypes.byref(unusual))
         finally:
-            if hptr:
-                lib.kpm_host_free(ctypes.c_void_p(hptr))
+            if dtext:
+                lib.kpm_device_free(ctx.handle, ctypes.c_void_p(dtext))
         _lib.check(rc, "parse_edges")
         for p in (du.value, dv.value, ds.value):
             bufs.add(p)
         if unusual.value:
             raise _NeedsHost()
         nlines = nl.value
+        t2 = time.perf_counter()
+        last_ingest_timing.update(parse_s=t2 - t1, lines=nlines)
         m, n = ctypes.c_int64(), ctypes.c_int64()
         eu, ev, dids = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
         info = (ctypes.c_int32 * 5)()
@@ -250,6 +321,8 @@ def _device_ingest(path, mm, allow_self_loops, ctx):
             ctypes.byref(ev), ctypes.byref(dids), info), "edges_finalize")
         for p in (eu.value, ev.value, dids.value):
             bufs.add(p)
+        t3 = time.perf_counter()
+        last_ingest_timing.update(finalize_s=t3 - t2)
         if info[0] & 2:
             raise _NeedsHost()  # ids Python's int() must judge ('_', > 18 digits)
         if info[3] != _INT32_MAX or (mm is not None and info[4]):
@@ -290,6 +363,7 @@ def _device_ingest(path, mm, allow_self_loops, ctx):
         _lib.check(lib.kpm_graph_from_edges(ctx.handle, n, eu, ev, m,
                                             1 if allow_self_loops else 0, ctypes.byref(h)),
                    "graph_from_edges")
+        last_ingest_timing.update(load_s=time.perf_counter() - t3, edges=m)
         return DeviceGraph(h.value, ctx), ids
 
 
