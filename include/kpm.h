@@ -273,6 +273,18 @@ int kpm_edges_finalize(kpm_ctx *ctx, int64_t n_lines, int64_t *u, int64_t *v,
                        int64_t *m, int64_t *n, int64_t **eu, int64_t **ev,
                        int64_t **ids, int32_t *info);
 
+/* ------------------------------------------ per-node histograms (§8f) --- */
+/* histogram_from_moments for per-node moments (density.py:63-108, the
+ * `coef @ table` product): masses[i][b] = sum_m (values[i][m]*damping[m]) *
+ * table[m][b]; norm[i] = values[i][0]*damping[0] (NULL damping = 1).
+ * values n x ld (ld >= m_max+1, e.g. the LDOS result left in HBM by
+ * kpm_run_result), table (m_max+1) x bins (cheb_bin_masses), masses n x bins:
+ * all host-or-device; norm (n) may be NULL.  *min_mass = min over all masses
+ * (NaN if any is NaN, as ndarray.min) for the negativity check. */
+int kpm_ldos_histogram(kpm_ctx *ctx, const double *values, int64_t n, int64_t ld,
+                       int32_t m_max, const double *damping, const double *table,
+                       int32_t bins, double *masses, double *norm, double *min_mass);
+
 #ifdef __cplusplus
 }
 #endif
