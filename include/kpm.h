@@ -285,6 +285,22 @@ int kpm_ldos_histogram(kpm_ctx *ctx, const double *values, int64_t n, int64_t ld
                        int32_t m_max, const double *damping, const double *table,
                        int32_t bins, double *masses, double *norm, double *min_mass);
 
+/* ------------------------------------------------ Lanczos (§8f row 4) --- */
+/* lanczos_factorize (lanczos.py:46-91) for k start vectors at once on the
+ * operator of g (explicit values or the implicit normalized adjacency, with
+ * its shift/scale: ScaledOperator.apply semantics).  z: n x ldz row-major
+ * (host-or-device), column c the start vector; z_norm[c] = ||z_c|| computed
+ * by the caller (q_0 = z / z_norm, as the reference).  Runs min(steps, n)
+ * iterations with two classical Gram-Schmidt passes against the whole basis.
+ * Host outputs: alphas k x S, betas k x (S-1) (S = min(steps, n)),
+ * taken[c] = iterations run, exhausted[c] = 1 on a vanishing residual
+ * (beta <= 1e-12 max(hnorm, 1e-300)), status[c] = 0 ok, 1 non-finite alpha,
+ * 2 non-finite residual (taken[c] is then the reference's `iterations`).
+ * basis (optional, host-or-device): k x S x n, vector-major. */
+int kpm_lanczos(kpm_graph *g, const double *z, int64_t ldz, int64_t k, int32_t steps,
+                const double *z_norm, double *alphas, double *betas, int32_t *taken,
+                int32_t *exhausted, int32_t *status, double *basis);
+
 #ifdef __cplusplus
 }
 #endif

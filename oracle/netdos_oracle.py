@@ -398,6 +398,50 @@ def histogram_masses(values, bins=50, damping=True, shift=0.0, scale=1.0,
     return edges, masses
 
 
+# ------------------------------------------------------------------ Lanczos
+def lanczos_factorize(apply, z, steps):
+    """lanczos.py:46-91: Lanczos from z with two classical Gram-Schmidt passes
+    against the whole basis; stops on a residual below 1e-12 * hnorm.
+    `apply(x)` is the operator's matvec.  Returns (alphas, betas, exhausted,
+    basis)."""
+    z = np.asarray(z, dtype=np.float64)
+    z_norm = float(np.linalg.norm(z))
+    n = z.shape[0]
+    steps = min(steps, n)
+    basis = np.empty((n, steps))
+    basis[:, 0] = z / z_norm
+    alphas, betas = np.empty(steps), np.empty(max(steps - 1, 0))
+    exhausted, hnorm, k = False, 0.0, 0
+    for j in range(steps):
+        q = basis[:, j]
+        w = apply(q)
+        alphas[j] = float(q @ w)
+        hnorm = max(hnorm, abs(alphas[j]) + (betas[j - 1] if j > 0 else 0.0))
+        k = j + 1
+        if j == steps - 1:
+            break
+        qb = basis[:, : j + 1]
+        for _ in range(2):
+            w -= qb @ (qb.T @ w)
+        beta = float(np.linalg.norm(w))
+        if beta <= 1e-12 * max(hnorm, 1e-300):
+            exhausted = True
+            break
+        betas[j] = beta
+        hnorm = max(hnorm, beta)
+        basis[:, j + 1] = w / beta
+    return alphas[:k].copy(), betas[: k - 1].copy(), exhausted, basis[:, :k].copy()
+
+
+def ritz_rule(alphas, betas):
+    """lanczos.py:104-119: Ritz nodes and first-component weights."""
+    from scipy.linalg import eigh_tridiagonal
+    if alphas.shape[0] == 1:
+        return alphas.copy(), np.ones(1)
+    nodes, vecs = eigh_tridiagonal(alphas, betas)
+    return nodes, vecs[0, :] ** 2
+
+
 # ---------------------------------------------------------- motif filtering
 def project_out(columns, vectors):
     """motifs.py:400-403: for each sparse (idx, val) in order,

@@ -102,6 +102,8 @@ SIGNATURES = {
                                  _c_vp, _c_vp]),
     "kpm_edges_finalize": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_vp, _c_int, _c_i64,
                                     _c_vp, _c_vp, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "kpm_lanczos": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i32, _c_vp, _c_vp, _c_vp, _c_vp,
+                             _c_vp, _c_vp, _c_vp]),
     "kpm_ldos_histogram": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i64, _c_i32, _c_vp, _c_vp, _c_i32,
                                     _c_vp, _c_vp, ctypes.POINTER(_c_dbl)]),
 }

@@ -16,6 +16,6 @@ wait
 for v in "$@"; do
   tag=${v%%:*}
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out/libkpm_$tag.so" \
-    kpm_capi.o kpm_graph.o kpm_gen.o kpm_motif.o kpm_ingest.o kpm_density.o /tmp/step_$tag.o -lcudart_static -Xcompiler -fPIC
+    kpm_capi.o kpm_graph.o kpm_gen.o kpm_motif.o kpm_ingest.o kpm_density.o kpm_lanczos.o /tmp/step_$tag.o -lcudart_static -Xcompiler -fPIC
 done
 ls "$out"
