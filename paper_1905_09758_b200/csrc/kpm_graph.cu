@@ -167,6 +167,22 @@ __global__ void dinv_kernel(const int64_t *__restrict__ row_ptr, int64_t n,
   if ((threadIdx.x & 31) == 0) atomicMax(max_deg, local);
 }
 
+// Rows per floor(log2(degree)) bucket (degree >= 1): the step kernel's L2
+// policy picks its "hot" (re-gathered) rows from it.
+__global__ void deg_hist_kernel(const int64_t *__restrict__ row_ptr, int64_t n,
+                                unsigned long long *__restrict__ hist) {
+  __shared__ unsigned long long sh[64];
+  if (threadIdx.x < 64) sh[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = row_ptr[i + 1] - row_ptr[i];
+    if (d > 0) atomicAdd(&sh[63 - __clzll((unsigned long long)d)], 1ull);
+  }
+  __syncthreads();
+  if (threadIdx.x < 64 && sh[threadIdx.x]) atomicAdd(hist + threadIdx.x, sh[threadIdx.x]);
+}
+
 // Chunk c covers rows [start[c], start[c+1]); boundaries split the prefix of
 // the per-row cost min(deg, heavy) + kRowCost evenly (heavy rows are worked
 // by their own CTAs, kpm_step.cu).  Depends on the graph only.
@@ -241,6 +257,15 @@ int finish_graph(kpm_graph *g) {
   unsigned long long hmax = 0;
   KPM_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof(hmax), cudaMemcpyDeviceToHost, st));
   KPM_CUDA(cudaFreeAsync(dmax, st));
+  {
+    unsigned long long *dh = nullptr;
+    KPM_CUDA(cudaMallocAsync(&dh, sizeof(unsigned long long) * 64, st));
+    KPM_CUDA(cudaMemsetAsync(dh, 0, sizeof(unsigned long long) * 64, st));
+    if (n > 0) deg_hist_kernel<<<grid_for(n), 256, 0, st>>>(g->row_ptr, n, dh);
+    KPM_CUDA(cudaMemcpyAsync(g->deg_log2_hist, dh, sizeof(unsigned long long) * 64,
+                             cudaMemcpyDeviceToHost, st));
+    KPM_CUDA(cudaFreeAsync(dh, st));
+  }
 
   // capped row costs -> prefix (n+1) ; heavy-row flags
   g->heavy_threshold = kHeavyDegree;

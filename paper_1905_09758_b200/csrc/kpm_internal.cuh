@@ -84,6 +84,8 @@ struct kpm_graph {
   // global).  dinv_all: d^-1/2 of all n_global rows (NULL = dinv, unpartitioned)
   int64_t row0 = 0, n_global = 0;
   double *dinv_all = nullptr;
+  // rows per floor(log2(degree)) bucket (finish_graph): hot-row L2 policy
+  unsigned long long deg_log2_hist[64] = {};
 };
 
 #define KPM_MAX_PARTS 16

@@ -26,6 +26,7 @@
 // column tile, so every gathered neighbour row is one coalesced 8*ld-byte
 // read; neighbour ids / weights are loaded 32 at a time by the lanes and
 // broadcast with shuffles, and U gathers are kept in flight per warp.
+#include <cmath>
 #include <cstdlib>
 
 #include "kpm_internal.cuh"
@@ -72,6 +73,8 @@ struct StepParams {
   const double *xparts[kMaxParts];
   int raw;                 // finalize writes raw sums (partitions combine on host)
   double *hpart;           // n_heavy x 2 x ld (global modes)
+  double hot_dinv;         // gathered rows with dinv_j <= hot_dinv are "hot" (L2 policy)
+  int bulk;                // 4-column layout: TMA bulk-copy gathers (light_bulk)
   double *hldos;           // n_heavy x n_slices (LDOS)
 };
 
@@ -239,6 +242,38 @@ __device__ __forceinline__ void ld_vec(const double *p, double (&v)[C]) {
   }
 }
 
+// Gather with an explicit L2 eviction policy (KPM_HOT_POLICY experiments):
+// rows of high-degree vertices are re-gathered many times per step, so they
+// are loaded with evict_last; the rest with evict_first (policy 2) or the
+// default policy (1).
+#ifndef KPM_HOT_POLICY
+#define KPM_HOT_POLICY 0
+#endif
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <int C>
+__device__ __forceinline__ void ld_vec_pol(const double *p, double (&v)[C], uint64_t pol) {
+  if constexpr (C == 1) {
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[0]) : "l"(p), "l"(pol));
+  } else if constexpr (C == 2) {
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
+  } else {
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v[2]), "=d"(v[3]) : "l"(p + 2), "l"(pol));
+  }
+}
+
 // plain (coherent) load: Xprev may alias Y
 // T_{k-1} is read exactly once per step (its last use before being
 // overwritten) and T_{k+1} is only read back next step: with KPM_STREAM_HINTS
@@ -351,8 +386,15 @@ __device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, doub
           double hl = 0.0;
           if (lane < cnt) {
             jl = p.col[base + lane];
-            if constexpr (EXPL) hl = p.vals[base + lane];
-            else hl = __dmul_rn(di, __ldg(p.dinv + jl));
+            if constexpr (EXPL) {
+              hl = p.vals[base + lane];
+            } else {
+              const double dj = __ldg(p.dinv + jl);
+              hl = __dmul_rn(di, dj);
+#if KPM_HOT_POLICY
+              if (dj <= p.hot_dinv) jl |= (int)0x80000000;
+#endif
+            }
           }
           for (int q = 0; q < cnt; q += U) {
             double v[U][C];
@@ -361,8 +403,19 @@ __device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, doub
               const int j = __shfl_sync(0xffffffffu, jl, (q + u) & 31);
 #pragma unroll
               for (int c = 0; c < C; ++c) v[u][c] = 0.0;
-              if (q + u < cnt && active)
+              if (q + u < cnt && active) {
+#if KPM_HOT_POLICY
+                const double *src = gather_row(p, (uint32_t)j & 0x7fffffffu) + c0;
+#if KPM_HOT_POLICY == 2
+                ld_vec_pol<C>(src, v[u], j < 0 ? l2_policy_last() : l2_policy_first());
+#else
+                if (j < 0) ld_vec_pol<C>(src, v[u], l2_policy_last());
+                else ld_vec<C>(src, v[u]);
+#endif
+#else
                 ld_vec<C>(gather_row(p, (uint32_t)j) + c0, v[u]);
+#endif
+              }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -662,6 +715,340 @@ __device__ __forceinline__ void light_stream(const StepParams &p, int chunk, dou
   }
 }
 
+// ------------------------------------------------ bulk-copy gathers (C = 4)
+// The same streamed light chunk for the 4-column layout (one column tile,
+// ld <= 128), with the neighbour rows moved by the TMA engine instead of
+// register loads: every gathered row (8*ld <= 1 KB) is one cp.async.bulk
+// global->shared copy completing on its own mbarrier, so the bytes in flight
+// per warp no longer cost registers.  A warp owns a ring of kBulkSlots row
+// slots; nonzeros are issued in waves of kBulkWave (lane L of the issuing
+// half-warp copies one row into slot L; one mbarrier per wave collects the
+// copies' bytes), kBulkSlots / kBulkWave waves are in flight, and the
+// consumer waits once per wave and adds the rows IN CSR ORDER from shared memory
+// (same products, same sequential sums => still bit-identical).  Neighbour ids
+// are loaded two batches ahead and their dinv_j one batch ahead, so neither
+// dependent load sits on the critical path.  Optional L2 policies: rows of
+// vertices with dinv_j <= hot_dinv (high degree, re-gathered many times per
+// step) are copied with evict_last, the rest with evict_first.
+#ifndef KPM_BULK_WAVE
+#define KPM_BULK_WAVE 8
+#endif
+constexpr int kBulkWave = KPM_BULK_WAVE;
+#ifndef KPM_BULK_SLOTS
+#define KPM_BULK_SLOTS 8
+#endif
+constexpr int kBulkSlots = KPM_BULK_SLOTS;
+static_assert(kBulkSlots % kBulkWave == 0 && kBulkSlots <= 32, "ring shape");
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void bulk_gather(void *dst, const void *src, uint32_t bytes,
+                                            uint64_t *bar, int pol_kind, uint64_t pol) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  if (pol_kind) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// Row epilogue of the bulk path: as stream_finish_row, with the moment
+// products folded into per-lane registers (the lane owns fixed columns).
+template <int MODE, bool EXPL, bool FIRST>
+__device__ __forceinline__ void bulk_finish_row(const StepParams &p, int row, bool active,
+                                                int64_t c0, const double (&acc)[4],
+                                                const double (&xo)[4], const double (&pv)[4],
+                                                const double (&zv)[4], double (&s1)[4],
+                                                double (&s2)[4]) {
+  constexpr int C = 4;
+  const int lane = threadIdx.x & 31;
+  double lsum = 0.0;
+  if (active) {
+    double y[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) y[c] = acc[c];
+    if constexpr (EXPL) {
+      if (p.shift != 0.0) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) y[c] = __dsub_rn(y[c], __dmul_rn(p.shift, xo[c]));
+      }
+      if (p.scale != 1.0) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) y[c] = __ddiv_rn(y[c], p.scale);
+      }
+    }
+    if constexpr (!FIRST) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) y[c] = __dsub_rn(__dmul_rn(2.0, y[c]), pv[c]);
+    }
+    st_vec<C>(p.Y + (size_t)row * p.ld + c0, y);
+    if constexpr (MODE == MODE_DBL) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        s1[c] = __dadd_rn(s1[c], __dmul_rn(y[c], xo[c]));
+        s2[c] = __dadd_rn(s2[c], __dmul_rn(y[c], y[c]));
+      }
+    } else if constexpr (MODE == MODE_DIRECT) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) s1[c] = __dadd_rn(s1[c], __dmul_rn(zv[c], y[c]));
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c) lsum = __dadd_rn(lsum, __dmul_rn(zv[c], y[c]));
+    }
+  }
+  if constexpr (MODE == MODE_LDOS) {
+    const double num = warp_sum_fixed(lsum);
+    if (lane == 0) {
+      if (!isfinite(num)) atomicOr(p.flag, 1);
+      p.ldos[(size_t)row * p.ldos_stride + p.ldos_col] = num;
+    }
+  }
+}
+
+struct BulkRing {
+  double *slot;     // kBulkSlots x ld doubles
+  double *wv;       // kBulkSlots: dinv_j (implicit) or the stored value
+  uint64_t *bar;    // one mbarrier per wave group (kBulkSlots / kBulkWave)
+  uint32_t phase;   // bit g: parity of group g's next completion (warp-uniform)
+};
+
+template <int MODE, bool EXPL, bool FIRST>
+__device__ __forceinline__ void light_bulk(const StepParams &p, int chunk, BulkRing &ring) {
+  constexpr int C = 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t ld = p.ld;
+  const int64_t c0 = (int64_t)lane * C;
+  const bool active = c0 < ld;
+  const uint32_t rbytes = (uint32_t)(ld * sizeof(double));
+  const int r0 = p.chunk_start[chunk], r1 = p.chunk_start[chunk + 1];
+  double s1[C], s2[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) s1[c] = s2[c] = 0.0;
+  if (r1 - r0 == 1 && p.n_heavy > 0 &&
+      p.row_ptr[r1] - p.row_ptr[r0] >= p.heavy_threshold) {
+    if constexpr (MODE != MODE_LDOS) {
+      double *out = p.partial + (size_t)chunk * 2 * ld;
+      for (int64_t e = lane; e < 2 * ld; e += 32) out[e] = 0.0;
+    }
+    return;
+  }
+  int wb = r0;
+  int64_t wrp = p.row_ptr[min(r0 + lane, r1)];
+  double wdi = 0.0;
+  if constexpr (!EXPL) wdi = (r0 + lane < r1) ? p.dinv[p.row0 + r0 + lane] : 0.0;
+  auto refill = [&](int base) {
+    wb = base;
+    wrp = p.row_ptr[min(base + lane, r1)];
+    if constexpr (!EXPL) wdi = (base + lane < r1) ? p.dinv[p.row0 + base + lane] : 0.0;
+  };
+  auto rp = [&](int r) { return __shfl_sync(0xffffffffu, wrp, r - wb); };
+  const int64_t K0 = __shfl_sync(0xffffffffu, wrp, 0);
+  const int64_t K1 = p.row_ptr[r1];
+  int row = r0;
+  if (row + 1 - wb > 31) refill(row);
+  int64_t rend = rp(row + 1);
+  double di = 0.0;
+  if constexpr (!EXPL) di = __shfl_sync(0xffffffffu, wdi, row - wb);
+  double xo[C], pv[C], zv[C];
+  auto own = [&](int r) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) xo[c] = pv[c] = zv[c] = 0.0;
+    if (r < r1 && active) {
+      const size_t off = (size_t)r * ld + c0;
+      if constexpr (EXPL || MODE == MODE_DBL) ld_vec<C>(p.X + off, xo);
+      if constexpr (!FIRST) ld_vec_rw<C>(p.Xprev + off, pv);
+      if constexpr (MODE != MODE_DBL) ld_vec<C>(p.Z + off, zv);
+    }
+  };
+  own(row);
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+  auto advance = [&](int64_t kk) {
+    while (row < r1 && kk == rend) {
+      bulk_finish_row<MODE, EXPL, FIRST>(p, row, active, c0, acc, xo, pv, zv, s1, s2);
+      ++row;
+      if (row >= r1) break;
+      if (row + 1 - wb > 31) refill(row);
+      rend = rp(row + 1);
+      if constexpr (!EXPL) di = __shfl_sync(0xffffffffu, wdi, row - wb);
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = 0.0;
+      own(row);
+    }
+  };
+  advance(K0);
+
+  // neighbour ids two batches ahead, dinv_j / values one batch ahead
+  const int64_t nnz = K1 - K0;
+  auto ld_col = [&](int64_t b) -> int {
+    const int64_t e = K0 + b * 32 + lane;
+    return e < K1 ? p.col[e] : 0;
+  };
+  auto ld_w = [&](int64_t b, int j) -> double {
+    const int64_t e = K0 + b * 32 + lane;
+    if (e >= K1) return 0.0;
+    if constexpr (EXPL) return p.vals[e];
+    else return __ldg(p.dinv + j);
+  };
+  int jc = ld_col(0), jn = ld_col(1), jnn = 0;
+  double wc = ld_w(0, jc), wn = 0.0;
+  int64_t cur_b = 0;  // batch held in (jc, wc)
+  const bool hints = p.hot_dinv > 0.0;
+  const uint64_t pol_last = hints ? l2_policy_last() : 0, pol_first = hints ? l2_policy_first() : 0;
+  auto issue = [&](int64_t w) {  // wave w -> slots (w % nw) * kBulkWave + k
+    const int64_t e0 = w * kBulkWave;
+    if (e0 >= nnz) return;
+    const int64_t b = e0 >> 5;
+    if (b != cur_b) {  // advance the batch registers (b == cur_b + 1)
+      jc = jn;
+      jn = jnn;
+      wc = wn;
+      cur_b = b;
+      jnn = ld_col(b + 2);
+      wn = ld_w(b + 1, jn);
+    } else if (b == 0 && w == 0) {
+      jnn = ld_col(2);
+      wn = ld_w(1, jn);
+    }
+    const int src_lane = (int)(e0 & 31) + (lane & (kBulkWave - 1));
+    const int j = __shfl_sync(0xffffffffu, jc, src_lane);
+    const double wv = __shfl_sync(0xffffffffu, wc, src_lane);
+    const int g = (int)(w % (kBulkSlots / kBulkWave));
+    const int base = g * kBulkWave;
+    const int k = lane - base;
+    if (k >= 0 && k < kBulkWave) {
+      // every lane of the group arrives (count kBulkWave); lanes with a
+      // nonzero also add their copy's bytes to the wave's transaction count
+      if (e0 + k < nnz) {
+        const int L = base + k;
+        ring.wv[L] = wv;
+        bool hot = false;
+        if constexpr (!EXPL) hot = wv <= p.hot_dinv;
+        bulk_gather(ring.slot + (size_t)L * ld, gather_row(p, (uint32_t)j), rbytes, ring.bar + g,
+                    hints ? 1 : 0, hot ? pol_last : pol_first);
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(ring.bar + g))
+                     : "memory");
+      }
+    }
+  };
+  constexpr int kWaves = kBulkSlots / kBulkWave;
+  const int64_t nwaves = (nnz + kBulkWave - 1) / kBulkWave;
+  // inactive lanes (c0 >= ld) read column 0 of the slot; their sums are unused
+  const uint32_t slot_sa = smem_u32(ring.slot) + (uint32_t)(active ? c0 : 0) * 8u;
+  const uint32_t wv_sa = smem_u32(ring.wv);
+#pragma unroll
+  for (int w = 0; w < kWaves; ++w) issue(w);
+  __syncwarp();
+  for (int64_t w = 0; w < nwaves; ++w) {
+    const int g = (int)(w % kWaves);
+    const int base = g * kBulkWave;
+    const int cnt = (int)min((int64_t)kBulkWave, nnz - w * kBulkWave);
+    mbar_wait(ring.bar + g, (ring.phase >> g) & 1u);  // the whole wave landed
+    ring.phase ^= 1u << g;
+    const int64_t e0 = K0 + w * kBulkWave;
+    // one neighbour: 32 B of the slot per lane + its weight (shared loads by
+    // 32-bit shared-window address, no generic->shared conversion per use)
+    auto add_one = [&](int L) {
+      double v[C];
+      const uint32_t a = slot_sa + (uint32_t)L * rbytes;
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a));
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + 16));
+      double wv;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wv) : "r"(wv_sa + 8u * (uint32_t)L));
+      double h;
+      if constexpr (EXPL) h = wv;
+      else h = __dmul_rn(di, wv);
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[c]));
+    };
+    if (cnt == kBulkWave && e0 + kBulkWave <= rend) {
+      // fast path: a full wave inside the current row, no row-end checks
+#pragma unroll
+      for (int k = 0; k < kBulkWave; ++k) add_one(base + k);
+      advance(e0 + kBulkWave);
+    } else {
+      for (int k = 0; k < cnt; ++k) {
+        add_one(base + k);
+        advance(e0 + k + 1);
+      }
+    }
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue(w + kWaves);
+    __syncwarp();
+  }
+  advance(K1);
+  if constexpr (MODE != MODE_LDOS) {
+    if (active) {
+      double *out = p.partial + (size_t)chunk * 2 * ld + c0;
+      st_vec<C>(out, s1);
+      if constexpr (MODE == MODE_DBL) st_vec<C>(out + ld, s2);
+    }
+  }
+}
+
+#ifndef KPM_BULK_THREADS
+#define KPM_BULK_THREADS 256
+#endif
+#ifndef KPM_BULK_MINB
+#define KPM_BULK_MINB 2
+#endif
+template <int MODE, bool EXPL, bool FIRST>
+__global__ void __launch_bounds__(KPM_BULK_THREADS, KPM_BULK_MINB)
+kpm_step_bulk_kernel(const StepParams p) {
+  extern __shared__ __align__(16) double sbulk[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t ld = p.ld;
+  // per warp: [kBulkSlots*ld ring][kBulkSlots values][kBulkSlots bars]
+  const size_t per_warp = (size_t)kBulkSlots * ld + kBulkSlots + kBulkSlots;
+  double *base = sbulk + (size_t)warp * per_warp;
+  BulkRing ring;
+  ring.slot = base;
+  ring.wv = ring.slot + (size_t)kBulkSlots * ld;
+  ring.bar = reinterpret_cast<uint64_t *>(ring.wv + kBulkSlots);
+  ring.phase = 0;
+  if (lane < kBulkSlots / kBulkWave) mbar_init(ring.bar + lane, kBulkWave);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  const int64_t total = p.n_heavy_tasks + p.n_chunks;
+  for (;;) {
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(p.queue, 1ull);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if ((int64_t)item >= total) break;
+    if ((int64_t)item < p.n_heavy_tasks) {
+      heavy_task<MODE, EXPL, FIRST>(p, (int64_t)item);
+      continue;
+    }
+    const int chunk = p.chunk_order[(int64_t)item - p.n_heavy_tasks];
+    light_bulk<MODE, EXPL, FIRST>(p, chunk, ring);
+  }
+}
+
 // Persistent fused step kernel.  Work items: [0, n_heavy_tasks) hub-row
 // slices in degree-descending order, then the light row chunks.  Warps grab
 // items from one atomic counter (dynamic load balance, hubs first); every item
@@ -819,9 +1206,43 @@ static int resident_blocks(K kern, size_t smem) {
   return nb;
 }
 
+template <int MODE>
+static cudaError_t launch_bulk(const kpm_run *r, const StepParams &p, bool expl, bool first,
+                               cudaStream_t st) {
+  void (*kern)(StepParams);
+  if (expl && first) kern = kpm_step_bulk_kernel<MODE, true, true>;
+  else if (expl) kern = kpm_step_bulk_kernel<MODE, true, false>;
+  else if (first) kern = kpm_step_bulk_kernel<MODE, false, true>;
+  else kern = kpm_step_bulk_kernel<MODE, false, false>;
+  const int threads = KPM_BULK_THREADS;
+  const size_t per_warp = (size_t)kBulkSlots * p.ld + 2 * kBulkSlots;
+  const size_t smem = (size_t)(threads / 32) * per_warp * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t items = p.n_chunks + p.n_heavy_tasks;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) != cudaSuccess ||
+      nb < 1) {
+    cudaGetLastError();
+    nb = 1;
+  }
+  int64_t grid = (int64_t)r->g->ctx->sm_count * nb;
+  const int64_t need = (items + threads / 32 - 1) / (threads / 32);
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, threads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
 template <int C, int MODE, bool INIT>
 static cudaError_t launch_c(const kpm_run *r, const StepParams &p, bool expl, bool first,
                             cudaStream_t st) {
+  if constexpr (C == 4 && !INIT) {
+    if (p.bulk && p.ld <= 128) return launch_bulk<MODE>(r, p, expl, first, st);
+  }
   constexpr int U = Tune<C>::u;
   const int threads = 256;
   size_t smem = (MODE == MODE_LDOS) ? 0 : (size_t)(threads / 32) * 2 * p.ld * sizeof(double);
@@ -907,6 +1328,24 @@ static StepParams base_params(const kpm_run *r) {
   p.hldos = r->hldos;
   p.stream = 1;
   if (const char *e = getenv("KPM_STREAM")) p.stream = atoi(e);
+  p.bulk = 1;  // KPM_BULK=0: register gathers for the 4-column layout too
+  if (const char *e = getenv("KPM_BULK")) p.bulk = atoi(e);
+  // hot rows (L2 evict_last in the bulk path): the highest-degree rows whose
+  // T_k rows fill at most kHotBytes of L2, by power-of-two degree class;
+  // KPM_HOT_DEGREE=<d> overrides (0 disables)
+  p.hot_dinv = -1.0;
+  {
+    constexpr double kHotBytes = 64.0 * 1024 * 1024;
+    const double budget = kHotBytes / (8.0 * (double)r->ld);
+    double rows = 0.0, hot_deg = 0.0;
+    for (int b = 63; b >= 0; --b) {
+      rows += (double)g->deg_log2_hist[b];
+      if (rows > budget) break;
+      hot_deg = std::ldexp(1.0, b);
+    }
+    if (const char *e = getenv("KPM_HOT_DEGREE")) hot_deg = atof(e);
+    if (hot_deg > 0) p.hot_dinv = 1.0 / sqrt(hot_deg);
+  }
   return p;
 }
 

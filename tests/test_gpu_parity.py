@@ -384,6 +384,56 @@ def test_hub_path_large_degree(oracle, kpm_ctx, monkeypatch):
     assert _normwise(c, want) <= 1e-12
 
 
+def _block_after(dev, z, mode, steps, ctx):
+    run = Run(dev, z.shape[1], mode, 2 * steps + 2)
+    run.set_probe_block(z, z.shape[1])
+    run.advance(steps)
+    ptr, ld, _ = run.block()
+    t = _d2h(ptr, (dev.n, ld), ctx)[:, : z.shape[1]]
+    run.free()
+    return t
+
+
+@pytest.mark.parametrize("P", [65, 100, 128])
+@pytest.mark.parametrize("mode", [_lib.MODE_DOS_DIRECT, _lib.MODE_DOS_DOUBLING,
+                                  _lib.MODE_LDOS])
+def test_bulk_gather_path_bitexact(oracle, kpm_ctx, monkeypatch, P, mode):
+    """The 4-column layout gathers neighbour rows with TMA bulk copies into a
+    shared-memory ring (light_bulk): T blocks bit-identical to the oracle's
+    restated recurrence and to the register-gather path, with and without the
+    hot-row L2 policy."""
+    g = kp.preferential_attachment(6000, 4, seed=9)
+    dev = g.device()
+    rp, ci, dinv = dev.export()
+    ci = ci.astype(np.int64)
+    z = oracle.make_probes(g.n, P, "rademacher", seed=P)
+    want = oracle.c_recurrence_block(rp, ci, oracle.normadj_values(rp, ci, dinv), z, 4,
+                                     threads=8)
+    got = {}
+    for bulk, hot in (("1", None), ("1", "4"), ("0", None)):
+        monkeypatch.setenv("KPM_BULK", bulk)
+        if hot:
+            monkeypatch.setenv("KPM_HOT_DEGREE", hot)
+        else:
+            monkeypatch.delenv("KPM_HOT_DEGREE", raising=False)
+        got[(bulk, hot)] = _block_after(dev, z, mode, 4, kpm_ctx)
+    for key, t in got.items():
+        assert np.array_equal(t, want), key
+
+
+def test_bulk_gather_rmat_moments_match_register_path(kpm_ctx, monkeypatch):
+    dev = kp.DeviceGraph.rmat(15, 16, seed=3)
+    sop = kp.rescale_operator(kp.NormalizedAdjacencyOperator(dev), (-1.0, 1.0))
+    z = kp.make_probes(dev.n, 128, "rademacher", seed=4)
+    monkeypatch.setenv("KPM_BULK", "1")
+    m1 = kp.dos_moments(sop, z, 40).values
+    h1 = kp.pdos_moments(sop, z, 12).values
+    monkeypatch.setenv("KPM_BULK", "0")
+    m0 = kp.dos_moments(sop, z, 40).values
+    h0 = kp.pdos_moments(sop, z, 12).values
+    assert np.array_equal(m0, m1) and np.array_equal(h0, h1)
+
+
 # ------------------------------------------------- device motif detection
 def _inst_key(i):
     return (i.kind.value, tuple(i.nodes), i.eigenvalue, i.multiplicity,
