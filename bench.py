@@ -280,8 +280,17 @@ def run_ours(args):
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "bytes_per_launch_model": bstep,
                          "bytes_per_launch_compulsory": _compulsory_bytes(n, nnz, P),
-                         "kernel": "kpm_step_kernel<C=4,DBL>", "kernel_ms": round(kern_avg, 4),
-                         "hbm_gbs_model_per_step": round(bstep / (ms_step * 1e-3) / 1e9, 1)},
+                         "kernel": ("kpm_step_bulk_kernel<DBL> (TMA bulk-copy gathers)"
+                                    if P > 64 and os.environ.get("KPM_BULK", "1") != "0"
+                                    else "kpm_step_kernel<DBL>"),
+                         "kernel_ms": round(kern_avg, 4),
+                         "hbm_gbs_model_per_step": round(bstep / (ms_step * 1e-3) / 1e9, 1),
+                         # measured DRAM bytes per launch (ncu, profiles/traffic.json)
+                         # over the live kernel time: the DRAM-side fraction
+                         "traffic_GBs": (round(traffic / (kern_avg * 1e-3) / 1e9, 1)
+                                         if traffic else None),
+                         "traffic_frac": (round(traffic / (kern_avg * 1e-3) / 1e9 / peak, 4)
+                                          if traffic else None)},
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 2 * args.steps,
             "clocks": clk.summary(),
