@@ -281,7 +281,7 @@ def run_ours(args):
                          "bytes_per_launch_model": bstep,
                          "bytes_per_launch_compulsory": _compulsory_bytes(n, nnz, P),
                          "kernel": ("kpm_step_bulk_kernel<DBL> (TMA bulk-copy gathers)"
-                                    if P > 64 and os.environ.get("KPM_BULK", "1") != "0"
+                                    if os.environ.get("KPM_BULK", "2") != "0"
                                     else "kpm_step_kernel<DBL>"),
                          "kernel_ms": round(kern_avg, 4),
                          "hbm_gbs_model_per_step": round(bstep / (ms_step * 1e-3) / 1e9, 1),

@@ -74,7 +74,7 @@ struct StepParams {
   int raw;                 // finalize writes raw sums (partitions combine on host)
   double *hpart;           // n_heavy x 2 x ld (global modes)
   double hot_dinv;         // gathered rows with dinv_j <= hot_dinv are "hot" (L2 policy)
-  int bulk;                // 4-column layout: TMA bulk-copy gathers (light_bulk)
+  int bulk;                // TMA bulk-copy gathers (light_bulk): 0 off, 1 C=4, 2 all
   double *hldos;           // n_heavy x n_slices (LDOS)
 };
 
@@ -737,8 +737,19 @@ constexpr int kBulkWave = KPM_BULK_WAVE;
 #ifndef KPM_BULK_SLOTS
 #define KPM_BULK_SLOTS 8
 #endif
-constexpr int kBulkSlots = KPM_BULK_SLOTS;
-static_assert(kBulkSlots % kBulkWave == 0 && kBulkSlots <= 32, "ring shape");
+#ifndef KPM_BULK_SLOTS2
+#define KPM_BULK_SLOTS2 16
+#endif
+#ifndef KPM_BULK_SLOTS1
+#define KPM_BULK_SLOTS1 32
+#endif
+// ring slots per warp for the 4-, 2- and 1-column layouts (rows of <= 1 KB,
+// 512 B, 256 B): about 8 KB of gathers in flight per warp in each case
+template <int C>
+struct BulkShape {
+  static constexpr int slots = C == 4 ? KPM_BULK_SLOTS : (C == 2 ? KPM_BULK_SLOTS2 : KPM_BULK_SLOTS1);
+  static_assert(slots % kBulkWave == 0 && slots <= 32, "ring shape");
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -774,13 +785,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 
 // Row epilogue of the bulk path: as stream_finish_row, with the moment
 // products folded into per-lane registers (the lane owns fixed columns).
-template <int MODE, bool EXPL, bool FIRST>
+template <int C, int MODE, bool EXPL, bool FIRST>
 __device__ __forceinline__ void bulk_finish_row(const StepParams &p, int row, bool active,
-                                                int64_t c0, const double (&acc)[4],
-                                                const double (&xo)[4], const double (&pv)[4],
-                                                const double (&zv)[4], double (&s1)[4],
-                                                double (&s2)[4]) {
-  constexpr int C = 4;
+                                                int64_t c0, const double (&acc)[C],
+                                                const double (&xo)[C], const double (&pv)[C],
+                                                const double (&zv)[C], double (&s1)[C],
+                                                double (&s2)[C]) {
   const int lane = threadIdx.x & 31;
   double lsum = 0.0;
   if (active) {
@@ -826,15 +836,15 @@ __device__ __forceinline__ void bulk_finish_row(const StepParams &p, int row, bo
 }
 
 struct BulkRing {
-  double *slot;     // kBulkSlots x ld doubles
-  double *wv;       // kBulkSlots: dinv_j (implicit) or the stored value
-  uint64_t *bar;    // one mbarrier per wave group (kBulkSlots / kBulkWave)
+  double *slot;     // slots x ld doubles
+  double *wv;       // slots: dinv_j (implicit) or the stored value
+  uint64_t *bar;    // one mbarrier per wave group (slots / kBulkWave)
   uint32_t phase;   // bit g: parity of group g's next completion (warp-uniform)
 };
 
-template <int MODE, bool EXPL, bool FIRST>
+template <int C, int MODE, bool EXPL, bool FIRST>
 __device__ __forceinline__ void light_bulk(const StepParams &p, int chunk, BulkRing &ring) {
-  constexpr int C = 4;
+  constexpr int kBulkSlots = BulkShape<C>::slots;
   const int lane = threadIdx.x & 31;
   const int64_t ld = p.ld;
   const int64_t c0 = (int64_t)lane * C;
@@ -886,7 +896,7 @@ __device__ __forceinline__ void light_bulk(const StepParams &p, int chunk, BulkR
   for (int c = 0; c < C; ++c) acc[c] = 0.0;
   auto advance = [&](int64_t kk) {
     while (row < r1 && kk == rend) {
-      bulk_finish_row<MODE, EXPL, FIRST>(p, row, active, c0, acc, xo, pv, zv, s1, s2);
+      bulk_finish_row<C, MODE, EXPL, FIRST>(p, row, active, c0, acc, xo, pv, zv, s1, s2);
       ++row;
       if (row >= r1) break;
       if (row + 1 - wb > 31) refill(row);
@@ -973,8 +983,13 @@ __device__ __forceinline__ void light_bulk(const StepParams &p, int chunk, BulkR
     auto add_one = [&](int L) {
       double v[C];
       const uint32_t a = slot_sa + (uint32_t)L * rbytes;
-      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a));
-      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + 16));
+      if constexpr (C == 1) {
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v[0]) : "r"(a));
+      } else {
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a));
+        if constexpr (C == 4)
+          asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + 16));
+      }
       double wv;
       asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wv) : "r"(wv_sa + 8u * (uint32_t)L));
       double h;
@@ -1015,9 +1030,20 @@ __device__ __forceinline__ void light_bulk(const StepParams &p, int chunk, BulkR
 #ifndef KPM_BULK_MINB
 #define KPM_BULK_MINB 2
 #endif
-template <int MODE, bool EXPL, bool FIRST>
-__global__ void __launch_bounds__(KPM_BULK_THREADS, KPM_BULK_MINB)
+#ifndef KPM_BULK_MINB2
+#define KPM_BULK_MINB2 3
+#endif
+#ifndef KPM_BULK_MINB1
+#define KPM_BULK_MINB1 2
+#endif
+template <int C>
+struct BulkTune {
+  static constexpr int minb = C == 4 ? KPM_BULK_MINB : (C == 2 ? KPM_BULK_MINB2 : KPM_BULK_MINB1);
+};
+template <int C, int MODE, bool EXPL, bool FIRST>
+__global__ void __launch_bounds__(KPM_BULK_THREADS, BulkTune<C>::minb)
 kpm_step_bulk_kernel(const StepParams p) {
+  constexpr int kBulkSlots = BulkShape<C>::slots;
   extern __shared__ __align__(16) double sbulk[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -1045,7 +1071,7 @@ kpm_step_bulk_kernel(const StepParams p) {
       continue;
     }
     const int chunk = p.chunk_order[(int64_t)item - p.n_heavy_tasks];
-    light_bulk<MODE, EXPL, FIRST>(p, chunk, ring);
+    light_bulk<C, MODE, EXPL, FIRST>(p, chunk, ring);
   }
 }
 
@@ -1206,14 +1232,15 @@ static int resident_blocks(K kern, size_t smem) {
   return nb;
 }
 
-template <int MODE>
+template <int C, int MODE>
 static cudaError_t launch_bulk(const kpm_run *r, const StepParams &p, bool expl, bool first,
                                cudaStream_t st) {
+  constexpr int kBulkSlots = BulkShape<C>::slots;
   void (*kern)(StepParams);
-  if (expl && first) kern = kpm_step_bulk_kernel<MODE, true, true>;
-  else if (expl) kern = kpm_step_bulk_kernel<MODE, true, false>;
-  else if (first) kern = kpm_step_bulk_kernel<MODE, false, true>;
-  else kern = kpm_step_bulk_kernel<MODE, false, false>;
+  if (expl && first) kern = kpm_step_bulk_kernel<C, MODE, true, true>;
+  else if (expl) kern = kpm_step_bulk_kernel<C, MODE, true, false>;
+  else if (first) kern = kpm_step_bulk_kernel<C, MODE, false, true>;
+  else kern = kpm_step_bulk_kernel<C, MODE, false, false>;
   const int threads = KPM_BULK_THREADS;
   const size_t per_warp = (size_t)kBulkSlots * p.ld + 2 * kBulkSlots;
   const size_t smem = (size_t)(threads / 32) * per_warp * sizeof(double);
@@ -1240,8 +1267,12 @@ static cudaError_t launch_bulk(const kpm_run *r, const StepParams &p, bool expl,
 template <int C, int MODE, bool INIT>
 static cudaError_t launch_c(const kpm_run *r, const StepParams &p, bool expl, bool first,
                             cudaStream_t st) {
-  if constexpr (C == 4 && !INIT) {
-    if (p.bulk && p.ld <= 128) return launch_bulk<MODE>(r, p, expl, first, st);
+  if constexpr (!INIT) {
+    // bulk-copy gathers for a single column tile; KPM_BULK: 0 off, 1 the
+    // 4-column layout only, 2 every layout (default)
+    // (bulk copies move multiples of 16 B: rows of an even number of doubles)
+    if (p.ld <= 32 * C && (p.ld & 1) == 0 && (C == 4 ? p.bulk >= 1 : p.bulk >= 2))
+      return launch_bulk<C, MODE>(r, p, expl, first, st);
   }
   constexpr int U = Tune<C>::u;
   const int threads = 256;
@@ -1328,7 +1359,7 @@ static StepParams base_params(const kpm_run *r) {
   p.hldos = r->hldos;
   p.stream = 1;
   if (const char *e = getenv("KPM_STREAM")) p.stream = atoi(e);
-  p.bulk = 1;  // KPM_BULK=0: register gathers for the 4-column layout too
+  p.bulk = 2;  // bulk-copy gathers in every layout (KPM_BULK=1: 4-column only, 0: none)
   if (const char *e = getenv("KPM_BULK")) p.bulk = atoi(e);
   // hot rows (L2 evict_last in the bulk path): the highest-degree rows whose
   // T_k rows fill at most kHotBytes of L2, by power-of-two degree class;

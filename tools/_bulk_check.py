@@ -31,11 +31,11 @@ ok = True
 graphs = {"er": kp.erdos_renyi(3000, 0.01, seed=1).device(), "ba": kp.preferential_attachment(20000, 4, seed=2).device(),
           "rmat16": kp.DeviceGraph.rmat(16, 16, seed=3)}
 for name, dev in graphs.items():
-    for P in (65, 100, 128):
+    for P in (5, 20, 32, 40, 64, 65, 100, 128):
         for mode in (0, 1, 2):
             a, oa = run_once(dev, P, mode, 5, 0)
-            b, ob = run_once(dev, P, mode, 5, 1)
-            c, oc = run_once(dev, P, mode, 5, 1, hot=50)
+            b, ob = run_once(dev, P, mode, 5, 2)
+            c, oc = run_once(dev, P, mode, 5, 2, hot=50)
             same = np.array_equal(a, b) and np.array_equal(a, c)
             if oa is not None:
                 same = same and np.array_equal(oa, ob) and np.array_equal(oa, oc)
