@@ -1270,8 +1270,11 @@ static cudaError_t launch_c(const kpm_run *r, const StepParams &p, bool expl, bo
   if constexpr (!INIT) {
     // bulk-copy gathers for a single column tile; KPM_BULK: 0 off, 1 the
     // 4-column layout only, 2 every layout (default)
-    // (bulk copies move multiples of 16 B: rows of an even number of doubles)
-    if (p.ld <= 32 * C && (p.ld & 1) == 0 && (C == 4 ? p.bulk >= 1 : p.bulk >= 2))
+    // (bulk copies move multiples of 16 B: rows of an even number of doubles;
+    // row-partitioned runs gather peer GPUs' blocks with plain loads -- the
+    // bulk path is only exercised single-device here)
+    if (p.ld <= 32 * C && (p.ld & 1) == 0 && p.nparts <= 1 &&
+        (C == 4 ? p.bulk >= 1 : p.bulk >= 2))
       return launch_bulk<C, MODE>(r, p, expl, first, st);
   }
   constexpr int U = Tune<C>::u;
