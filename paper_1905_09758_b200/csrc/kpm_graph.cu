@@ -187,6 +187,7 @@ __global__ void deg_hist_kernel(const int64_t *__restrict__ row_ptr, int64_t n,
 // the per-row cost min(deg, heavy) + kRowCost evenly (heavy rows are worked
 // by their own CTAs, kpm_step.cu).  Depends on the graph only.
 static constexpr int64_t kRowCost = 8;
+static constexpr int64_t kMaxChunkCost = 16384;
 
 __global__ void row_cost_kernel(const int64_t *__restrict__ row_ptr, int64_t n,
                                 int64_t heavy, int64_t *__restrict__ cost,
@@ -294,7 +295,13 @@ int finish_graph(kpm_graph *g) {
   KPM_CUDA(cudaStreamSynchronize(st));
   // a fixed denominator (148 SMs x 128) keeps chunks independent of the device
   // and of the probe count, so reductions are reproducible.
+  // Big graphs cap the chunk cost instead (more chunks): the last chunks of
+  // the queue set the launch's tail, so a chunk must stay short next to the
+  // step (C5: 14 ms chunks at 148*128 of them, profiles/r01_trace_report.json).
   int64_t target = (total + 148 * 128 - 1) / (148 * 128);
+  int64_t cap = kMaxChunkCost;
+  if (const char *e = getenv("KPM_CHUNK_COST")) cap = atoll(e);
+  if (cap > 0 && target > cap) target = cap;
   if (target < 256) target = 256;
   int64_t nch = (total + target - 1) / target;
   if (nch < 1) nch = 1;

@@ -1,5 +1,6 @@
 // Internal types and helpers shared by the libkpm translation units.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -125,4 +126,8 @@ struct kpm_run {
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // pairs (start, stop), reused
   int32_t ev_used = 0;
+  // TMA tensor maps of the two recurrence blocks (n x ld fp64, box ld x 1) for
+  // the gather4 light path (kpm_step.cu light_g4); tm_ok when encodable
+  CUtensorMap tm[2];
+  bool tm_ok = false;
 };

@@ -76,7 +76,28 @@ struct StepParams {
   double hot_dinv;         // gathered rows with dinv_j <= hot_dinv are "hot" (L2 policy)
   int bulk;                // TMA bulk-copy gathers (light_bulk): 0 off, 1 C=4, 2 all
   double *hldos;           // n_heavy x n_slices (LDOS)
+  int g4;                  // TMA gather4 light path: 0 off, 1 for C <= 2, 2 all layouts
+  int lean;                // per-lane async gathers for C <= 2 (light_lean)
+  int64_t hub_off;         // dynamic smem (doubles) of warp 0's hub ring (kpm_step_kernel)
+  unsigned long long *trace;  // KPM_TRACE: per work item (start ns, end ns, smid<<32|warp)
 };
+
+// KPM_TRACE diagnostics: one record per work item of one traced launch
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_item(const StepParams &p, unsigned long long item,
+                                           unsigned long long t0) {
+  if (p.trace && (threadIdx.x & 31) == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    p.trace[3 * item] = t0;
+    p.trace[3 * item + 1] = gtimer();
+    p.trace[3 * item + 2] = ((unsigned long long)smid << 32) | (threadIdx.x >> 5);
+  }
+}
 
 // Address of gathered row j (global id) in the current T_k block.
 __device__ __forceinline__ const double *gather_row(const StepParams &p, uint32_t j) {
@@ -87,41 +108,45 @@ __device__ __forceinline__ const double *gather_row(const StepParams &p, uint32_
   return p.xparts[o] + (size_t)(j - (uint32_t)p.part_lo[o]) * (uint32_t)p.ld;
 }
 
-// Heavy rows are cut into 16-column slices; one warp owns one (row, slice)
-// task.  Lane (nb = lane/4, cg = lane%4) gathers 4 columns of neighbour nb of
-// an 8-neighbour wave, forms the products h_ij * X[j, c] in parallel, and the
-// products are then added IN NEIGHBOUR ORDER through shuffles, so every
-// (row, column) sum keeps the reference's sequential order (bit-exact) while
-// 32 neighbours' gathers are in flight per warp and a hub's slices run on
-// different SMs.
-constexpr int kSlice = 16;
+// Hub rows (degree >= heavy_threshold) are cut into kSlice-column slices and
+// one warp owns one (row, slice) task.  Its serial chain -- every (row, column)
+// sum is added in CSR order, bit-exact with the reference's _row -- is as long
+// as the hub's degree, so the task is a deep software pipeline: lane
+// (nb = lane/4, cg = lane%4) copies column cg of neighbour nb of each
+// 8-neighbour wave into its own shared-memory slot with cp.async (LDGSTS),
+// together with the wave's col ids (2*kHubDepth waves ahead) and dinv_j / the
+// stored value (kHubDepth waves ahead).  A lane only reads back what it copied
+// itself, so one per-thread cp.async group per wave is the whole
+// synchronisation, and 8*kHubDepth neighbours stay in flight per warp (the
+// former register-gather version waited one memory latency per 32 neighbours
+// and set the launch length on R-MAT: the 406k-degree hub of C3 took the whole
+// 52.7 ms step at P = 32, profiles/r01_trace_report.json).  Products h_ij*X[j,c] are
+// formed in parallel and added in neighbour order through shuffles.
+constexpr int kSlice = 4;
+constexpr int kHubDepth = 16;
+// per-warp hub ring: rows [kHubDepth][32] + dinv_j [kHubDepth][8] doubles,
+// col ids [2*kHubDepth][8] int32
+constexpr int kHubRingDoubles = kHubDepth * 32 + kHubDepth * 8 + kHubDepth * 8;
 
-__device__ __forceinline__ void ld4_masked(const double *p, int64_t avail, bool vec,
-                                           double (&v)[4]) {
-  if (vec) {
-    double2 t0 = __ldg(reinterpret_cast<const double2 *>(p));
-    double2 t1 = __ldg(reinterpret_cast<const double2 *>(p + 2));
-    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
-  } else {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) v[c] = c < avail ? __ldg(p + c) : 0.0;
-  }
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
-
-__device__ __forceinline__ void ld4_rw_masked(const double *p, int64_t avail, bool vec,
-                                              double (&v)[4]) {
-  if (vec) {
-    double2 t0 = *reinterpret_cast<const double2 *>(p);
-    double2 t1 = *reinterpret_cast<const double2 *>(p + 2);
-    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
-  } else {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) v[c] = c < avail ? p[c] : 0.0;
-  }
+__device__ __forceinline__ void cp_async_8(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_4(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 template <int MODE, bool EXPL, bool FIRST>
-__device__ __forceinline__ void heavy_task(const StepParams &p, int64_t t) {
+__device__ __forceinline__ void heavy_task(const StepParams &p, int64_t t, double *hub) {
   const int lane = threadIdx.x & 31;
   const int nb = lane >> 2, cg = lane & 3;
   const int64_t ld = p.ld;
@@ -129,101 +154,101 @@ __device__ __forceinline__ void heavy_task(const StepParams &p, int64_t t) {
   const int h = (int)(t / nsl), sl = (int)(t % nsl);
   const int i = p.heavy_rows[h];
   const int64_t beg = p.row_ptr[i], end = p.row_ptr[i + 1];
+  const int64_t d = end - beg;
   double di = 0.0;
   if constexpr (!EXPL) di = p.dinv[p.row0 + i];
-  const int64_t c0 = (int64_t)sl * kSlice + cg * 4;
-  const int64_t avail = ld - c0;  // columns of this lane inside the row
-  const bool active = avail > 0;
-  const bool vec = (ld & 3) == 0;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t base = beg; base < end; base += 32) {
-    const int cnt = (int)min((int64_t)32, end - base);
-    int jl = 0;
-    double hl = 0.0;
-    if (lane < cnt) {
-      jl = p.col[base + lane];
-      if constexpr (EXPL) hl = p.vals[base + lane];
-      else hl = __dmul_rn(di, __ldg(p.dinv + jl));
+  const int64_t c = (int64_t)sl * kSlice + cg;
+  const bool active = c < ld;
+  const uint32_t rows_sa = smem_u32(hub);                     // [D][32] doubles
+  const uint32_t w_sa = rows_sa + kHubDepth * 32 * 8;         // [D][8] doubles
+  const uint32_t col_sa = w_sa + kHubDepth * 8 * 8;           // [2D][8] int32
+  const int64_t nw = (d + 7) >> 3;
+  auto col_slot = [&](int64_t w) {
+    return col_sa + (uint32_t)(((w % (2 * kHubDepth)) * 8 + nb) * 4);
+  };
+  // col id of neighbour nb of wave w (lane nb*4 copies it)
+  auto issue_col = [&](int64_t w) {
+    const int64_t e = beg + w * 8 + nb;
+    if (cg == 0 && e < end) cp_async_4(col_slot(w), p.col + e);
+  };
+  // column c of neighbour nb of wave w, and its weight (col ids landed)
+  auto issue_row = [&](int64_t w) {
+    if (w >= nw) return;  // warp-uniform
+    const int64_t e = beg + w * 8 + nb;
+    int j = 0;
+    if (cg == 0 && e < end) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(j) : "r"(col_slot(w)));
+    j = __shfl_sync(0xffffffffu, j, lane & ~3);
+    if (e < end) {
+      const uint32_t slot = (uint32_t)(w % kHubDepth);
+      if (active) cp_async_8(rows_sa + (slot * 32 + lane) * 8, gather_row(p, (uint32_t)j) + c);
+      if (cg == 0) {
+        if constexpr (EXPL) cp_async_8(w_sa + (slot * 8 + nb) * 8, p.vals + e);
+        else cp_async_8(w_sa + (slot * 8 + nb) * 8, p.dinv + j);
+      }
     }
-    double v[4][4], hv[4];
-    int jw[4];
+  };
+  for (int w = 0; w < 2 * kHubDepth; ++w) issue_col(w);
+  cp_async_commit();
+  cp_async_wait<0>();
+  for (int w = 0; w < kHubDepth; ++w) {
+    issue_row(w);
+    cp_async_commit();
+  }
+  double acc = 0.0;
+  for (int64_t w = 0; w < nw; ++w) {
+    cp_async_wait<kHubDepth - 1>();  // wave w's rows / weights and col(w + D) landed
+    const uint32_t slot = (uint32_t)(w % kHubDepth);
+    double x = 0.0, wv = 0.0;
+    if (active) asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(rows_sa + (slot * 32 + lane) * 8));
+    if (cg == 0) asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wv) : "r"(w_sa + (slot * 8 + nb) * 8));
+    wv = __shfl_sync(0xffffffffu, wv, lane & ~3);
+    double hh;
+    if constexpr (EXPL) hh = wv;
+    else hh = __dmul_rn(di, wv);  // (1*dinv_i)*dinv_j, operators.py:110
+    const double prod = __dmul_rn(hh, x);
+    const int64_t cnt = d - w * 8;
+    if (cnt >= 8) {
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      jw[w] = __shfl_sync(0xffffffffu, jl, w * 8 + nb);
-      hv[w] = __shfl_sync(0xffffffffu, hl, w * 8 + nb);
-    }
-    // all four waves' gathers in flight before any is consumed
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) v[w][c] = 0.0;
-      if (w * 8 + nb < cnt && active)
-        ld4_masked(gather_row(p, (uint32_t)jw[w]) + c0, avail, vec, v[w]);
-    }
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) v[w][c] = __dmul_rn(hv[w], v[w][c]);
-    }
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
+      for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, prod, u * 4 + cg));
+    } else {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if (w * 8 + u < cnt) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            acc[c] = __dadd_rn(acc[c], __shfl_sync(0xffffffffu, v[w][c], u * 4 + cg));
-        }
+        const double v = __shfl_sync(0xffffffffu, prod, u * 4 + cg);
+        if (u < cnt) acc = __dadd_rn(acc, v);
       }
     }
+    issue_row(w + kHubDepth);
+    issue_col(w + 2 * kHubDepth);
+    cp_async_commit();
   }
-  // epilogue on lanes 0..3 (every lane holds the same sums for its cg)
+  cp_async_wait<0>();
+  // epilogue on lanes 0..3 (lane cg holds the sum of column c)
   double part = 0.0;
   if (nb == 0 && active) {
-    const size_t off = (size_t)i * ld + c0;
-    double y[4], xo[4], pv[4], zv[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) y[c] = acc[c];
-    if constexpr (EXPL || MODE == MODE_DBL) ld4_masked(p.X + off, avail, vec, xo);
+    const size_t off = (size_t)i * ld + c;
+    double y = acc, xo = 0.0;
+    if constexpr (EXPL || MODE == MODE_DBL) xo = __ldg(p.X + off);
     if constexpr (EXPL) {
-      if (p.shift != 0.0) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) y[c] = __dsub_rn(y[c], __dmul_rn(p.shift, xo[c]));
-      }
-      if (p.scale != 1.0) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) y[c] = __ddiv_rn(y[c], p.scale);
-      }
+      if (p.shift != 0.0) y = __dsub_rn(y, __dmul_rn(p.shift, xo));
+      if (p.scale != 1.0) y = __ddiv_rn(y, p.scale);
     }
-    if constexpr (!FIRST) {
-      ld4_rw_masked(p.Xprev + off, avail, vec, pv);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) y[c] = __dsub_rn(__dmul_rn(2.0, y[c]), pv[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      if (c < avail) p.Y[off + c] = y[c];
-    if constexpr (MODE != MODE_DBL) ld4_masked(p.Z + off, avail, vec, zv);
-    double *hp = p.hpart + (size_t)h * 2 * ld + c0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (c < avail) {
-        if constexpr (MODE == MODE_DBL) {
-          hp[c] = __dmul_rn(y[c], xo[c]);
-          hp[ld + c] = __dmul_rn(y[c], y[c]);
-        } else if constexpr (MODE == MODE_DIRECT) {
-          hp[c] = __dmul_rn(zv[c], y[c]);
-        } else {
-          part = __dadd_rn(part, __dmul_rn(zv[c], y[c]));
-        }
-      }
+    if constexpr (!FIRST) y = __dsub_rn(__dmul_rn(2.0, y), p.Xprev[off]);
+    p.Y[off] = y;
+    double *hp = p.hpart + (size_t)h * 2 * ld + c;
+    if constexpr (MODE == MODE_DBL) {
+      hp[0] = __dmul_rn(y, xo);
+      hp[ld] = __dmul_rn(y, y);
+    } else if constexpr (MODE == MODE_DIRECT) {
+      hp[0] = __dmul_rn(__ldg(p.Z + off), y);
+    } else {
+      part = __dmul_rn(__ldg(p.Z + off), y);
     }
   }
   if constexpr (MODE == MODE_LDOS) {
-    // slice sum over the 4 column groups in order (lanes 0..3)
+    // slice sum over its columns in order (lanes 0..3)
     double tot = __shfl_sync(0xffffffffu, part, 0);
 #pragma unroll
-    for (int g2 = 1; g2 < 4; ++g2) tot = __dadd_rn(tot, __shfl_sync(0xffffffffu, part, g2));
+    for (int g2 = 1; g2 < kSlice; ++g2) tot = __dadd_rn(tot, __shfl_sync(0xffffffffu, part, g2));
     if (lane == 0) p.hldos[(size_t)h * nsl + sl] = tot;
   }
 }
@@ -751,9 +776,6 @@ struct BulkShape {
   static_assert(slots % kBulkWave == 0 && slots <= 32, "ring shape");
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -833,6 +855,13 @@ __device__ __forceinline__ void bulk_finish_row(const StepParams &p, int row, bo
       p.ldos[(size_t)row * p.ldos_stride + p.ldos_col] = num;
     }
   }
+}
+
+// per-warp data region of the bulk kernel: the gather ring + weights, or the
+// hub ring when hub tasks exist (whichever is larger); the mbarriers follow
+__host__ __device__ inline size_t bulk_data_doubles(int slots, int64_t ld, bool hubs) {
+  const size_t ring = (size_t)slots * ld + slots;
+  return hubs && ring < (size_t)kHubRingDoubles ? (size_t)kHubRingDoubles : ring;
 }
 
 struct BulkRing {
@@ -955,7 +984,9 @@ __device__ __forceinline__ void light_bulk(const StepParams &p, int chunk, BulkR
         ring.wv[L] = wv;
         bool hot = false;
         if constexpr (!EXPL) hot = wv <= p.hot_dinv;
-        bulk_gather(ring.slot + (size_t)L * ld, gather_row(p, (uint32_t)j), rbytes, ring.bar + g,
+        bulk_gather(ring.slot + (size_t)L * ld,
+                    p.nparts <= 1 ? p.X + (size_t)(uint32_t)j * (uint32_t)ld : gather_row(p, (uint32_t)j),
+                    rbytes, ring.bar + g,
                     hints ? 1 : 0, hot ? pol_last : pol_first);
       } else {
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(ring.bar + g))
@@ -1048,13 +1079,13 @@ kpm_step_bulk_kernel(const StepParams p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t ld = p.ld;
-  // per warp: [kBulkSlots*ld ring][kBulkSlots values][kBulkSlots bars]
-  const size_t per_warp = (size_t)kBulkSlots * ld + kBulkSlots + kBulkSlots;
-  double *base = sbulk + (size_t)warp * per_warp;
+  // per warp: [kBulkSlots*ld ring][kBulkSlots values] (or the hub ring) [kBulkSlots bars]
+  const size_t data = bulk_data_doubles(kBulkSlots, ld, p.n_heavy_tasks > 0);
+  double *base = sbulk + (size_t)warp * (data + kBulkSlots);
   BulkRing ring;
   ring.slot = base;
   ring.wv = ring.slot + (size_t)kBulkSlots * ld;
-  ring.bar = reinterpret_cast<uint64_t *>(ring.wv + kBulkSlots);
+  ring.bar = reinterpret_cast<uint64_t *>(base + data);
   ring.phase = 0;
   if (lane < kBulkSlots / kBulkWave) mbar_init(ring.bar + lane, kBulkWave);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1066,12 +1097,576 @@ kpm_step_bulk_kernel(const StepParams p) {
     if (lane == 0) item = atomicAdd(p.queue, 1ull);
     item = __shfl_sync(0xffffffffu, item, 0);
     if ((int64_t)item >= total) break;
+    const unsigned long long t0 = p.trace ? gtimer() : 0;
     if ((int64_t)item < p.n_heavy_tasks) {
-      heavy_task<MODE, EXPL, FIRST>(p, (int64_t)item);
-      continue;
+      heavy_task<MODE, EXPL, FIRST>(p, (int64_t)item, base);
+    } else {
+      const int chunk = p.chunk_order[(int64_t)item - p.n_heavy_tasks];
+      light_bulk<C, MODE, EXPL, FIRST>(p, chunk, ring);
     }
-    const int chunk = p.chunk_order[(int64_t)item - p.n_heavy_tasks];
-    light_bulk<C, MODE, EXPL, FIRST>(p, chunk, ring);
+    trace_item(p, item, t0);
+  }
+}
+
+// ------------------------------------- per-lane async gathers (C <= 2)
+// Small probe blocks (P <= 64: one or two columns per lane, one column tile).
+// Here a neighbour row is only 256-512 B, so the bulk path's per-copy cost (a
+// uniform-register waterfall of ~9 instructions per cp.async.bulk) dominated:
+// ~34 warp instructions per nonzero at P = 32, issue-bound (ncu,
+// profiles/r01_ncu_summary.md).  This path moves every neighbour row with ONE
+// cp.async (LDGSTS) per warp -- lane l copies its own C columns into its own
+// slot -- so a lane reads back only what it copied.  Per wave of 8 nonzeros:
+// the wave's col ids (lanes 0..7, 2*D waves ahead) and dinv_j / stored values
+// (lanes 0..7, D waves ahead) ride in the same per-thread cp.async groups; the
+// consumer waits for the group of D waves ago, __syncwarp()s (the weights were
+// copied by other lanes) and adds the 8 rows IN CSR ORDER (bit-identical sums).
+// The rows' own operands (T_k, T_{k-1}, z) come through an R-row prefetch ring
+// completed on one mbarrier per slot (cp.async.mbarrier.arrive.noinc), so short
+// and empty rows no longer wait one memory latency each.
+template <int C, int MODE, bool EXPL, bool FIRST>
+struct Lean {
+  static constexpr int D = 4 / C;  // waves of 8 gathered rows in flight (8 KB)
+  static constexpr int R = 8 / C;  // own-row prefetch depth
+  static constexpr int NOP = ((EXPL || MODE == MODE_DBL) ? 1 : 0) + (FIRST ? 0 : 1) +
+                             (MODE != MODE_DBL ? 1 : 0);
+  static constexpr int W = 32 * C;  // doubles of one row tile
+  static constexpr int rows_d = D * 8 * W;
+  static constexpr int wv_d = D * 8;
+  static constexpr int col_d = D * 8;  // [2D][8] int32
+  static constexpr int own_d = R * (NOP > 0 ? NOP : 1) * W;
+  static constexpr int bar_d = R;
+  static constexpr int data_d = rows_d + wv_d + col_d + own_d + bar_d;
+  static constexpr int warp_d = data_d > kHubRingDoubles ? data_d : kHubRingDoubles;
+  static_assert(rows_d >= kHubRingDoubles, "hub ring must not reach the mbarriers");
+};
+
+template <int C>
+__device__ __forceinline__ void cp_async_cols(uint32_t dst, const double *src) {
+  if constexpr (C == 1) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+  } else {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    if constexpr (C == 4)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(src + 2)
+                   : "memory");
+  }
+}
+template <int C>
+__device__ __forceinline__ void lds_cols(uint32_t a, double (&v)[C]) {
+  if constexpr (C == 1) {
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v[0]) : "r"(a));
+  } else {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(a));
+    if constexpr (C == 4)
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(a + 16));
+  }
+}
+
+template <int C, int MODE, bool EXPL, bool FIRST>
+__device__ __forceinline__ void light_lean(const StepParams &p, int chunk, double *base,
+                                           uint32_t &ophase) {
+  using L = Lean<C, MODE, EXPL, FIRST>;
+  constexpr int D = L::D, R = L::R, W = L::W, NOP = L::NOP;
+  const int lane = threadIdx.x & 31;
+  const int64_t ld = p.ld;
+  const int64_t c0 = (int64_t)lane * C;
+  const bool active = c0 < ld;
+  const int r0 = p.chunk_start[chunk], r1 = p.chunk_start[chunk + 1];
+  double s1[C], s2[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) s1[c] = s2[c] = 0.0;
+  if (r1 - r0 == 1 && p.n_heavy > 0 &&
+      p.row_ptr[r1] - p.row_ptr[r0] >= p.heavy_threshold) {
+    if constexpr (MODE != MODE_LDOS) {
+      double *out = p.partial + (size_t)chunk * 2 * ld;
+      for (int64_t e = lane; e < 2 * ld; e += 32) out[e] = 0.0;
+    }
+    return;
+  }
+  const uint32_t rows_sa = smem_u32(base);
+  const uint32_t wv_sa = rows_sa + L::rows_d * 8;
+  const uint32_t col_sa = wv_sa + L::wv_d * 8;
+  const uint32_t own_sa = col_sa + L::col_d * 8;
+  uint64_t *obar = reinterpret_cast<uint64_t *>(base + L::rows_d + L::wv_d + L::col_d + L::own_d);
+
+  int wb = r0;
+  int64_t wrp = p.row_ptr[min(r0 + lane, r1)];
+  double wdi = 0.0;
+  if constexpr (!EXPL) wdi = (r0 + lane < r1) ? p.dinv[p.row0 + r0 + lane] : 0.0;
+  auto refill = [&](int b) {
+    wb = b;
+    wrp = p.row_ptr[min(b + lane, r1)];
+    if constexpr (!EXPL) wdi = (b + lane < r1) ? p.dinv[p.row0 + b + lane] : 0.0;
+  };
+  auto rp = [&](int r) { return __shfl_sync(0xffffffffu, wrp, r - wb); };
+  const int64_t K0 = __shfl_sync(0xffffffffu, wrp, 0);
+  const int64_t K1 = p.row_ptr[r1];
+  const int64_t nnz = K1 - K0;
+  const int64_t nw = (nnz + 7) >> 3;
+
+  // own operands of row r -> ring slot (r - r0) % R
+  auto issue_own = [&](int r) {
+    if (r >= r1) return;  // warp-uniform
+    const int sl = (r - r0) & (R - 1);
+    if (active) {
+      const size_t off = (size_t)r * ld + c0;
+      const uint32_t dst = own_sa + (uint32_t)(sl * NOP * W + lane * C) * 8;
+      int q = 0;
+      if constexpr (EXPL || MODE == MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.X + off);
+      if constexpr (!FIRST) cp_async_cols<C>(dst + (q++) * W * 8, p.Xprev + off);
+      if constexpr (MODE != MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.Z + off);
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(obar + sl))
+                 : "memory");
+  };
+  auto col_slot = [&](int64_t w) { return col_sa + (uint32_t)((w % (2 * D)) * 32); };
+  auto issue_col = [&](int64_t w) {
+    const int64_t e = w * 8 + lane;
+    if (lane < 8 && e < nnz) cp_async_4(col_slot(w) + lane * 4, p.col + K0 + e);
+  };
+  auto issue_rows = [&](int64_t w) {
+    if (w >= nw) return;  // warp-uniform
+    const uint32_t sl = (uint32_t)(w % D);
+    const int cnt = (int)min((int64_t)8, nnz - w * 8);
+    int j[8];
+    const uint32_t ca = col_slot(w);
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(j[0]), "=r"(j[1]), "=r"(j[2]), "=r"(j[3]) : "r"(ca));
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(j[4]), "=r"(j[5]), "=r"(j[6]), "=r"(j[7]) : "r"(ca + 16));
+    const uint32_t dst = rows_sa + (uint32_t)(sl * 8 * W + lane * C) * 8;
+    if (active) {
+      if (p.nparts <= 1) {  // hoisted: the partition lookup costs ~25 instructions per row
+        const double *xc = p.X + c0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < cnt) cp_async_cols<C>(dst + (uint32_t)(k * W) * 8, xc + (size_t)(uint32_t)j[k] * (uint32_t)ld);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < cnt) cp_async_cols<C>(dst + (uint32_t)(k * W) * 8, gather_row(p, (uint32_t)j[k]) + c0);
+      }
+    }
+    if (lane < cnt) {
+      const uint32_t wd = wv_sa + (sl * 8 + lane) * 8;
+      if constexpr (EXPL) {
+        cp_async_8(wd, p.vals + K0 + w * 8 + lane);
+      } else {
+        int jl;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jl) : "r"(ca + lane * 4));
+        cp_async_8(wd, p.dinv + jl);
+      }
+    }
+  };
+
+  // col ids of the first 2D waves, then the own rows and the first D waves
+#pragma unroll
+  for (int w = 0; w < 2 * D; ++w) issue_col(w);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < R; ++r) issue_own(r0 + r);
+#pragma unroll
+  for (int w = 0; w < D; ++w) {
+    issue_rows(w);
+    cp_async_commit();
+  }
+
+  int row = r0;
+  if (row + 1 - wb > 31) refill(row);
+  int64_t rend = rp(row + 1) - K0;  // nonzero positions relative to K0
+  double di = 0.0;
+  if constexpr (!EXPL) di = __shfl_sync(0xffffffffu, wdi, row - wb);
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+  auto finish = [&](int r) {
+    const int sl = (r - r0) & (R - 1);
+    mbar_wait(obar + sl, (ophase >> sl) & 1u);
+    ophase ^= 1u << sl;
+    double xo[C], pv[C], zv[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) xo[c] = pv[c] = zv[c] = 0.0;
+    if (active) {
+      const uint32_t a = own_sa + (uint32_t)(sl * NOP * W + lane * C) * 8;
+      int q = 0;
+      if constexpr (EXPL || MODE == MODE_DBL) lds_cols<C>(a + (q++) * W * 8, xo);
+      if constexpr (!FIRST) lds_cols<C>(a + (q++) * W * 8, pv);
+      if constexpr (MODE != MODE_DBL) lds_cols<C>(a + (q++) * W * 8, zv);
+    }
+    bulk_finish_row<C, MODE, EXPL, FIRST>(p, r, active, c0, acc, xo, pv, zv, s1, s2);
+    issue_own(r + R);
+  };
+  auto advance = [&](int64_t kk) {
+    while (row < r1 && kk == rend) {
+      finish(row);
+      ++row;
+      if (row >= r1) break;
+      if (row + 1 - wb > 31) refill(row);
+      rend = rp(row + 1) - K0;
+      if constexpr (!EXPL) di = __shfl_sync(0xffffffffu, wdi, row - wb);
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = 0.0;
+    }
+  };
+  advance(0);  // leading empty rows
+
+  const uint32_t my_rows = rows_sa + (uint32_t)(lane * C) * 8;
+  for (int64_t w = 0; w < nw; ++w) {
+    cp_async_wait<D - 1>();  // wave w's rows + weights, col ids of wave w + D
+    __syncwarp();
+    const uint32_t sl = (uint32_t)(w % D);
+    const int64_t e0 = w * 8;
+    const int cnt = (int)min((int64_t)8, nnz - e0);
+    auto add_one = [&](int k) {
+      double v[C];
+      lds_cols<C>(my_rows + (uint32_t)((sl * 8 + k) * W) * 8, v);
+      double wv;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wv) : "r"(wv_sa + (sl * 8 + k) * 8));
+      double h;
+      if constexpr (EXPL) h = wv;
+      else h = __dmul_rn(di, wv);  // (1*dinv_i)*dinv_j, operators.py:110
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[c]));
+    };
+    if (cnt == 8 && e0 + 8 <= rend) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) add_one(k);
+      advance(e0 + 8);
+    } else {
+      for (int k = 0; k < cnt; ++k) {
+        add_one(k);
+        advance(e0 + k + 1);
+      }
+    }
+    __syncwarp();  // every lane is done with the wave's weights
+    issue_rows(w + D);
+    issue_col(w + 2 * D);
+    cp_async_commit();
+  }
+  advance(nnz);
+  cp_async_wait<0>();
+  if constexpr (MODE != MODE_LDOS) {
+    if (active) {
+      double *out = p.partial + (size_t)chunk * 2 * ld + c0;
+      st_vec<C>(out, s1);
+      if constexpr (MODE == MODE_DBL) st_vec<C>(out + ld, s2);
+    }
+  }
+}
+
+#ifndef KPM_LEAN_MINB
+#define KPM_LEAN_MINB 2
+#endif
+template <int C, int MODE, bool EXPL, bool FIRST>
+__global__ void __launch_bounds__(256, KPM_LEAN_MINB) kpm_step_lean_kernel(const StepParams p) {
+  using L = Lean<C, MODE, EXPL, FIRST>;
+  extern __shared__ __align__(16) double slean[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double *base = slean + (size_t)warp * L::warp_d;
+  uint64_t *obar = reinterpret_cast<uint64_t *>(base + L::rows_d + L::wv_d + L::col_d + L::own_d);
+  if (lane < L::R) mbar_init(obar + lane, 32);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  uint32_t ophase = 0;
+  const int64_t total = p.n_heavy_tasks + p.n_chunks;
+  for (;;) {
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(p.queue, 1ull);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if ((int64_t)item >= total) break;
+    const unsigned long long t0 = p.trace ? gtimer() : 0;
+    if ((int64_t)item < p.n_heavy_tasks) {
+      heavy_task<MODE, EXPL, FIRST>(p, (int64_t)item, base);
+    } else {
+      const int chunk = p.chunk_order[(int64_t)item - p.n_heavy_tasks];
+      light_lean<C, MODE, EXPL, FIRST>(p, chunk, base, ophase);
+    }
+    trace_item(p, item, t0);
+  }
+}
+
+// ------------------------------------------------ TMA gather4 light path
+// The gathered neighbour rows are moved by the tensor engine's row gather:
+// ONE cp.async.bulk.tensor...tile::gather4 (SASS UTMALDG.2D.GATHER4) copies
+// four whole rows of the T_k block (tensor map n x ld fp64, box ld x 1) into
+// the warp's ring, issued by lane 0 -- no per-lane copies, no uniform-register
+// waterfall per row.  A wave is WAVE neighbours (WAVE/4 gather4 ops) completing
+// on one mbarrier: lane 0 arrives with expect_tx for the rows, lanes 0..WAVE-1
+// copy dinv_j / the stored value and the col ids of the wave 2D ahead with
+// cp.async and arrive through cp.async.mbarrier.arrive.noinc, so a completed
+// wave also has the col ids of the wave its slot is refilled with.  The
+// consumer adds the rows IN CSR ORDER from shared memory (bit-identical sums);
+// own operands come through the light_lean prefetch ring.
+#ifndef KPM_G4_WAVE1
+#define KPM_G4_WAVE1 16
+#endif
+template <int C, int MODE, bool EXPL, bool FIRST>
+struct G4 {
+  static constexpr int WAVE = C == 1 ? KPM_G4_WAVE1 : (C == 2 ? 8 : 4);  // neighbours per wave
+  static constexpr int D = 32 / (WAVE * C);  // waves in flight: 8 KB of rows
+  static constexpr int R = C == 4 ? 2 : 8 / C;  // own-row prefetch depth
+  static constexpr int NOP = Lean<C, MODE, EXPL, FIRST>::NOP;
+  static constexpr int W = 32 * C;
+  static constexpr int slot_d = ((WAVE * W * 8 + 127) / 128) * 128 / 8;  // one wave's rows
+  static constexpr int rows_d = D * slot_d;
+  static constexpr int wv_d = D * WAVE;
+  static constexpr int col_d = D * WAVE;  // [2D][WAVE] int32
+  static constexpr int own_d = R * (NOP > 0 ? NOP : 1) * W;
+  static constexpr int bar_d = D + R;
+  static constexpr int data_d = rows_d + wv_d + col_d + own_d;
+  static constexpr int warp_d = ((data_d > kHubRingDoubles ? data_d : kHubRingDoubles) + bar_d + 15) / 16 * 16;
+};
+
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm, int j0, int j1,
+                                            int j2, int j3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(tm), "r"(0), "r"(j0), "r"(j1), "r"(j2), "r"(j3), "r"(bar)
+      : "memory");
+}
+
+template <int C, int MODE, bool EXPL, bool FIRST>
+__device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap *tm, int chunk,
+                                         double *base, uint32_t &ophase, uint32_t &wphase) {
+  using L = G4<C, MODE, EXPL, FIRST>;
+  constexpr int D = L::D, R = L::R, W = L::W, NOP = L::NOP, WAVE = L::WAVE;
+  const int lane = threadIdx.x & 31;
+  const int64_t ld = p.ld;
+  const int64_t c0 = (int64_t)lane * C;
+  const bool active = c0 < ld;
+  const int r0 = p.chunk_start[chunk], r1 = p.chunk_start[chunk + 1];
+  double s1[C], s2[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) s1[c] = s2[c] = 0.0;
+  if (r1 - r0 == 1 && p.n_heavy > 0 &&
+      p.row_ptr[r1] - p.row_ptr[r0] >= p.heavy_threshold) {
+    if constexpr (MODE != MODE_LDOS) {
+      double *out = p.partial + (size_t)chunk * 2 * ld;
+      for (int64_t e = lane; e < 2 * ld; e += 32) out[e] = 0.0;
+    }
+    return;
+  }
+  const uint32_t rows_sa = smem_u32(base);
+  const uint32_t wv_sa = rows_sa + L::rows_d * 8;
+  const uint32_t col_sa = wv_sa + L::wv_d * 8;
+  const uint32_t own_sa = col_sa + L::col_d * 8;
+  uint64_t *wbar = reinterpret_cast<uint64_t *>(base + L::warp_d - L::bar_d);
+  uint64_t *obar = wbar + D;
+  const uint32_t rbytes = (uint32_t)ld * 8u;
+
+  int wb = r0;
+  int64_t wrp = p.row_ptr[min(r0 + lane, r1)];
+  double wdi = 0.0;
+  if constexpr (!EXPL) wdi = (r0 + lane < r1) ? p.dinv[p.row0 + r0 + lane] : 0.0;
+  auto refill = [&](int b) {
+    wb = b;
+    wrp = p.row_ptr[min(b + lane, r1)];
+    if constexpr (!EXPL) wdi = (b + lane < r1) ? p.dinv[p.row0 + b + lane] : 0.0;
+  };
+  auto rp = [&](int r) { return __shfl_sync(0xffffffffu, wrp, r - wb); };
+  const int64_t K0 = __shfl_sync(0xffffffffu, wrp, 0);
+  const int64_t K1 = p.row_ptr[r1];
+  const int nnz = (int)(K1 - K0);  // a light chunk holds < 2^31 nonzeros
+  const int nw = (nnz + WAVE - 1) / WAVE;
+
+  auto issue_own = [&](int r) {
+    if (r >= r1) return;  // warp-uniform
+    const int sl = (r - r0) & (R - 1);
+    if (active) {
+      const size_t off = (size_t)r * ld + c0;
+      const uint32_t dst = own_sa + (uint32_t)(sl * NOP * W + lane * C) * 8;
+      int q = 0;
+      if constexpr (EXPL || MODE == MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.X + off);
+      if constexpr (!FIRST) cp_async_cols<C>(dst + (q++) * W * 8, p.Xprev + off);
+      if constexpr (MODE != MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.Z + off);
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(obar + sl))
+                 : "memory");
+  };
+  auto col_slot = [&](int w) { return col_sa + (uint32_t)((w % (2 * D)) * WAVE * 4); };
+  auto issue_col = [&](int w) {
+    const int e = w * WAVE + lane;
+    if (lane < WAVE && e < nnz) cp_async_4(col_slot(w) + lane * 4, p.col + K0 + e);
+  };
+  // wave w: rows by gather4 (lane 0), weights by lanes < cnt; the caller then
+  // lets lanes < WAVE arrive (noinc) after also issuing col(w + D)
+  auto issue_wave = [&](int w) {
+    const uint32_t sl = (uint32_t)(w % D);
+    const int cnt = min(WAVE, nnz - w * WAVE);
+    const uint32_t ca = col_slot(w);
+    const uint32_t bar = smem_u32(wbar + sl);
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads of the slot
+      int j[WAVE];
+#pragma unroll
+      for (int q = 0; q < WAVE / 4; ++q)
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(j[4 * q]), "=r"(j[4 * q + 1]), "=r"(j[4 * q + 2]), "=r"(j[4 * q + 3])
+                     : "r"(ca + 16 * q));
+#pragma unroll
+      for (int k = 1; k < WAVE; ++k)
+        if (k >= cnt) j[k] = j[0];  // a valid row; its bytes land unused
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"((uint32_t)WAVE * rbytes)
+                   : "memory");
+      const uint32_t dst = rows_sa + sl * (uint32_t)(L::slot_d * 8);
+#pragma unroll
+      for (int q = 0; q < WAVE / 4; ++q)
+        tma_gather4(dst + 4 * q * rbytes, tm, j[4 * q], j[4 * q + 1], j[4 * q + 2], j[4 * q + 3], bar);
+    }
+    if (lane < cnt) {
+      const uint32_t wd = wv_sa + (sl * WAVE + lane) * 8;
+      if constexpr (EXPL) {
+        cp_async_8(wd, p.vals + K0 + w * WAVE + lane);
+      } else {
+        int jl;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jl) : "r"(ca + lane * 4));
+        cp_async_8(wd, p.dinv + jl);
+      }
+    }
+  };
+  auto arrive_wave = [&](int w) {
+    if (lane < WAVE)
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                       smem_u32(wbar + (uint32_t)(w % D)))
+                   : "memory");
+  };
+
+#pragma unroll
+  for (int w = 0; w < 2 * D; ++w) issue_col(w);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < R; ++r) issue_own(r0 + r);
+#pragma unroll
+  for (int w = 0; w < D; ++w) {
+    if (w < nw) {
+      issue_wave(w);
+      arrive_wave(w);
+    }
+  }
+
+  int row = r0;
+  if (row + 1 - wb > 31) refill(row);
+  int64_t rend = rp(row + 1) - K0;
+  double di = 0.0;
+  if constexpr (!EXPL) di = __shfl_sync(0xffffffffu, wdi, row - wb);
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+  auto finish = [&](int r) {
+    const int sl = (r - r0) & (R - 1);
+    mbar_wait(obar + sl, (ophase >> sl) & 1u);
+    ophase ^= 1u << sl;
+    double xo[C], pv[C], zv[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) xo[c] = pv[c] = zv[c] = 0.0;
+    if (active) {
+      const uint32_t a = own_sa + (uint32_t)(sl * NOP * W + lane * C) * 8;
+      int q = 0;
+      if constexpr (EXPL || MODE == MODE_DBL) lds_cols<C>(a + (q++) * W * 8, xo);
+      if constexpr (!FIRST) lds_cols<C>(a + (q++) * W * 8, pv);
+      if constexpr (MODE != MODE_DBL) lds_cols<C>(a + (q++) * W * 8, zv);
+    }
+    bulk_finish_row<C, MODE, EXPL, FIRST>(p, r, active, c0, acc, xo, pv, zv, s1, s2);
+    issue_own(r + R);
+  };
+  auto advance = [&](int64_t kk) {
+    while (row < r1 && kk == rend) {
+      finish(row);
+      ++row;
+      if (row >= r1) break;
+      if (row + 1 - wb > 31) refill(row);
+      rend = rp(row + 1) - K0;
+      if constexpr (!EXPL) di = __shfl_sync(0xffffffffu, wdi, row - wb);
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = 0.0;
+    }
+  };
+  advance(0);
+
+  const uint32_t my_col = (uint32_t)(active ? c0 : 0) * 8u;
+  for (int w = 0; w < nw; ++w) {
+    const uint32_t sl = (uint32_t)(w % D);
+    mbar_wait(wbar + sl, (wphase >> sl) & 1u);
+    wphase ^= 1u << sl;
+    const int e0 = w * WAVE;
+    const int cnt = min(WAVE, nnz - e0);
+    const uint32_t slot = rows_sa + sl * (uint32_t)(L::slot_d * 8) + my_col;
+    auto add_one = [&](int k) {
+      double v[C];
+      lds_cols<C>(slot + k * rbytes, v);
+      double wv;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wv) : "r"(wv_sa + (sl * WAVE + k) * 8));
+      double h;
+      if constexpr (EXPL) h = wv;
+      else h = __dmul_rn(di, wv);  // (1*dinv_i)*dinv_j, operators.py:110
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[c]));
+    };
+    if (cnt == WAVE && e0 + WAVE <= rend) {
+#pragma unroll
+      for (int k = 0; k < WAVE; ++k) add_one(k);
+      advance(e0 + WAVE);
+    } else {
+      for (int k = 0; k < cnt; ++k) {
+        add_one(k);
+        advance(e0 + k + 1);
+      }
+    }
+    __syncwarp();  // the whole warp is done with the slot and its weights
+    if (w + D < nw) {
+      issue_wave(w + D);
+      issue_col(w + 2 * D);
+      arrive_wave(w + D);
+    }
+  }
+  advance(nnz);
+  if constexpr (MODE != MODE_LDOS) {
+    if (active) {
+      double *out = p.partial + (size_t)chunk * 2 * ld + c0;
+      st_vec<C>(out, s1);
+      if constexpr (MODE == MODE_DBL) st_vec<C>(out + ld, s2);
+    }
+  }
+}
+
+#ifndef KPM_G4_MINB
+#define KPM_G4_MINB 2
+#endif
+template <int C, int MODE, bool EXPL, bool FIRST>
+__global__ void __launch_bounds__(256, KPM_G4_MINB)
+kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
+  using L = G4<C, MODE, EXPL, FIRST>;
+  extern __shared__ __align__(128) double sg4[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double *base = sg4 + (size_t)warp * L::warp_d;
+  uint64_t *wbar = reinterpret_cast<uint64_t *>(base + L::warp_d - L::bar_d);
+  if (lane < L::D) mbar_init(wbar + lane, 1 + L::WAVE);
+  else if (lane < L::D + L::R) mbar_init(wbar + lane, 32);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  uint32_t ophase = 0, wphase = 0;
+  const int64_t total = p.n_heavy_tasks + p.n_chunks;
+  for (;;) {
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(p.queue, 1ull);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if ((int64_t)item >= total) break;
+    const unsigned long long t0 = p.trace ? gtimer() : 0;
+    if ((int64_t)item < p.n_heavy_tasks) {
+      heavy_task<MODE, EXPL, FIRST>(p, (int64_t)item, base);
+    } else {
+      const int chunk = p.chunk_order[(int64_t)item - p.n_heavy_tasks];
+      light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, base, ophase, wphase);
+    }
+    trace_item(p, item, t0);
   }
 }
 
@@ -1123,9 +1718,11 @@ kpm_step_kernel(const StepParams p) {
     if (lane == 0) item = atomicAdd(p.queue, 1ull);
     item = __shfl_sync(0xffffffffu, item, 0);
     if ((int64_t)item >= total) break;
+    const unsigned long long t0 = p.trace ? gtimer() : 0;
     if constexpr (!INIT) {
       if ((int64_t)item < n_heavy_tasks) {
-        heavy_task<MODE, EXPL, FIRST>(p, (int64_t)item);
+        heavy_task<MODE, EXPL, FIRST>(p, (int64_t)item, sacc + p.hub_off + (size_t)warp * kHubRingDoubles);
+        trace_item(p, item, t0);
         continue;
       }
     }
@@ -1134,11 +1731,13 @@ kpm_step_kernel(const StepParams p) {
       if constexpr (C <= KPM_STREAM_MAXC) {
         if (p.stream && p.ld <= 32 * C) {
           light_stream<C, MODE, EXPL, FIRST, U>(p, chunk, my);
+          trace_item(p, item, t0);
           continue;
         }
       }
     }
     light_chunk<C, MODE, EXPL, FIRST, INIT, U>(p, chunk, my);
+    trace_item(p, item, t0);
   }
 }
 
@@ -1242,7 +1841,7 @@ static cudaError_t launch_bulk(const kpm_run *r, const StepParams &p, bool expl,
   else if (first) kern = kpm_step_bulk_kernel<C, MODE, false, true>;
   else kern = kpm_step_bulk_kernel<C, MODE, false, false>;
   const int threads = KPM_BULK_THREADS;
-  const size_t per_warp = (size_t)kBulkSlots * p.ld + 2 * kBulkSlots;
+  const size_t per_warp = bulk_data_doubles(kBulkSlots, p.ld, p.n_heavy_tasks > 0) + kBulkSlots;
   const size_t smem = (size_t)(threads / 32) * per_warp * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
@@ -1264,9 +1863,89 @@ static cudaError_t launch_bulk(const kpm_run *r, const StepParams &p, bool expl,
   return cudaGetLastError();
 }
 
+template <int C, int MODE, bool EXPL, bool FIRST>
+static cudaError_t launch_lean_k(const kpm_run *r, const StepParams &p, cudaStream_t st) {
+  void (*kern)(StepParams) = kpm_step_lean_kernel<C, MODE, EXPL, FIRST>;
+  const int threads = 256;
+  const size_t smem = (size_t)(threads / 32) * Lean<C, MODE, EXPL, FIRST>::warp_d * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t items = p.n_chunks + p.n_heavy_tasks;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) != cudaSuccess ||
+      nb < 1) {
+    cudaGetLastError();
+    nb = 1;
+  }
+  int64_t grid = (int64_t)r->g->ctx->sm_count * nb;
+  const int64_t need = (items + threads / 32 - 1) / (threads / 32);
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, threads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int C, int MODE, bool EXPL, bool FIRST>
+static cudaError_t launch_g4_k(const kpm_run *r, const StepParams &p, const CUtensorMap &tm,
+                               cudaStream_t st) {
+  void (*kern)(StepParams, CUtensorMap) = kpm_step_g4_kernel<C, MODE, EXPL, FIRST>;
+  const int threads = 256;
+  const size_t smem = (size_t)(threads / 32) * G4<C, MODE, EXPL, FIRST>::warp_d * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t items = p.n_chunks + p.n_heavy_tasks;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) != cudaSuccess ||
+      nb < 1) {
+    cudaGetLastError();
+    nb = 1;
+  }
+  int64_t grid = (int64_t)r->g->ctx->sm_count * nb;
+  const int64_t need = (items + threads / 32 - 1) / (threads / 32);
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, threads, smem, st>>>(p, tm);
+  return cudaGetLastError();
+}
+
+template <int C, int MODE>
+static cudaError_t launch_g4(const kpm_run *r, const StepParams &p, bool expl, bool first,
+                             cudaStream_t st) {
+  const CUtensorMap &tm = r->tm[p.X == r->a ? 0 : 1];
+  if (expl && first) return launch_g4_k<C, MODE, true, true>(r, p, tm, st);
+  if (expl) return launch_g4_k<C, MODE, true, false>(r, p, tm, st);
+  if (first) return launch_g4_k<C, MODE, false, true>(r, p, tm, st);
+  return launch_g4_k<C, MODE, false, false>(r, p, tm, st);
+}
+
+template <int C, int MODE>
+static cudaError_t launch_lean(const kpm_run *r, const StepParams &p, bool expl, bool first,
+                               cudaStream_t st) {
+  if (expl && first) return launch_lean_k<C, MODE, true, true>(r, p, st);
+  if (expl) return launch_lean_k<C, MODE, true, false>(r, p, st);
+  if (first) return launch_lean_k<C, MODE, false, true>(r, p, st);
+  return launch_lean_k<C, MODE, false, false>(r, p, st);
+}
+
 template <int C, int MODE, bool INIT>
 static cudaError_t launch_c(const kpm_run *r, const StepParams &p, bool expl, bool first,
                             cudaStream_t st) {
+  if constexpr (!INIT) {
+    // TMA gather4 for one column tile (tensor maps of both blocks encoded)
+    if (p.ld <= 32 * C && p.g4 >= (C == 4 ? 2 : 1) && r->tm_ok && p.nparts <= 1 &&
+        (p.X == r->a || p.X == r->b))
+      return launch_g4<C, MODE>(r, p, expl, first, st);
+  }
+  if constexpr (!INIT && C <= 2) {
+    // per-lane async gathers for one column tile of 1 or 2 columns per lane
+    if (p.ld <= 32 * C && p.lean) return launch_lean<C, MODE>(r, p, expl, first, st);
+  }
   if constexpr (!INIT) {
     // bulk-copy gathers for a single column tile; KPM_BULK: 0 off, 1 the
     // 4-column layout only, 2 every layout (default)
@@ -1280,6 +1959,9 @@ static cudaError_t launch_c(const kpm_run *r, const StepParams &p, bool expl, bo
   constexpr int U = Tune<C>::u;
   const int threads = 256;
   size_t smem = (MODE == MODE_LDOS) ? 0 : (size_t)(threads / 32) * 2 * p.ld * sizeof(double);
+  StepParams q = p;  // + one hub ring per warp after the accumulators
+  q.hub_off = (int64_t)(smem / sizeof(double));
+  if (!INIT && p.n_heavy_tasks > 0) smem += (size_t)(threads / 32) * kHubRingDoubles * sizeof(double);
   void (*kern)(StepParams);
   if (INIT) kern = kpm_step_kernel<C, MODE, false, true, true, U>;
   else if (expl && first) kern = kpm_step_kernel<C, MODE, true, true, false, U>;
@@ -1298,7 +1980,7 @@ static cudaError_t launch_c(const kpm_run *r, const StepParams &p, bool expl, bo
   if (grid < 1) grid = 1;
   cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)grid, threads, smem, st>>>(p);
+  kern<<<(unsigned)grid, threads, smem, st>>>(q);
   return cudaGetLastError();
 }
 
@@ -1362,6 +2044,10 @@ static StepParams base_params(const kpm_run *r) {
   p.hldos = r->hldos;
   p.stream = 1;
   if (const char *e = getenv("KPM_STREAM")) p.stream = atoi(e);
+  p.g4 = 1;  // TMA gather4 light path for the 1- and 2-column layouts (KPM_G4=2: also 4)
+  if (const char *e = getenv("KPM_G4")) p.g4 = atoi(e);
+  p.lean = 1;  // per-lane async gathers for the 1- and 2-column layouts (KPM_LEAN=0: off)
+  if (const char *e = getenv("KPM_LEAN")) p.lean = atoi(e);
   p.bulk = 2;  // bulk-copy gathers in every layout (KPM_BULK=1: 4-column only, 0: none)
   if (const char *e = getenv("KPM_BULK")) p.bulk = atoi(e);
   // hot rows (L2 evict_last in the bulk path): the highest-degree rows whose
@@ -1531,6 +2217,42 @@ __global__ void filter_kernel(double *__restrict__ z, int64_t k, int64_t ldz,
 
 using namespace kpm;
 
+// Tensor maps of the recurrence blocks for the gather4 path: n x ld fp64,
+// row stride 8*ld, box ld x 1 (ld <= 128, a multiple of 4).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static void encode_block_maps(kpm_run *r) {
+  r->tm_ok = false;
+  const kpm_graph *g = r->g;
+  // ld % 4 == 0 keeps the second gather4 of a wave 128-byte aligned in shared memory
+  if (g->n < 1 || g->n >= (int64_t)1 << 31 || (r->ld & 3) || r->ld > 128 || !r->a || !r->b) return;
+  static EncodeTiledFn enc = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&enc, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      enc = nullptr;
+    cudaGetLastError();
+  }
+  if (!enc) return;
+  const cuuint64_t dims[2] = {(cuuint64_t)r->ld, (cuuint64_t)g->n};
+  const cuuint64_t strides[1] = {(cuuint64_t)r->ld * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)r->ld, 1};
+  const cuuint32_t es[2] = {1, 1};
+  double *blk[2] = {r->a, r->b};
+  for (int q = 0; q < 2; ++q)
+    if (enc(&r->tm[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, blk[q], dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return;
+  r->tm_ok = true;
+}
+
 extern "C" {
 
 int kpm_run_create(kpm_graph *g, int64_t k, int32_t mode, int32_t m_max,
@@ -1562,7 +2284,7 @@ int kpm_run_create(kpm_graph *g, int64_t k, int32_t mode, int32_t m_max,
   A((void **)&r->flag, sizeof(int32_t) * 4);
   A((void **)&r->queue, sizeof(unsigned long long));
   const int64_t nh = g->n_heavy > 0 ? g->n_heavy : 1;
-  if (mode == KPM_MODE_LDOS) A((void **)&r->hldos, sizeof(double) * nh * ((r->ld + 15) / 16));
+  if (mode == KPM_MODE_LDOS) A((void **)&r->hldos, sizeof(double) * nh * ((r->ld + kSlice - 1) / kSlice));
   else A((void **)&r->hpart, sizeof(double) * nh * 2 * r->ld);
   if (mode == KPM_MODE_LDOS) {
     A((void **)&r->ldos, sizeof(double) * (size_t)(g->n > 0 ? g->n : 1) * (m_max + 1));
@@ -1573,6 +2295,7 @@ int kpm_run_create(kpm_graph *g, int64_t k, int32_t mode, int32_t m_max,
       sizeof(double) * (size_t)((g->n_chunks + 31) / 32 + 1) * 2 * r->ld);
     A((void **)&r->contrib, sizeof(double) * (size_t)(m_max + 1) * r->ld);
   }
+  if (e == cudaSuccess) encode_block_maps(r);
   if (e != cudaSuccess) {
     cudaGetLastError();
     kpm_run_free(r);
@@ -1692,7 +2415,43 @@ int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
       }
       KPM_CUDA(cudaEventRecord(r->ev[2 * r->ev_used], st));
     }
+    // KPM_TRACE=<file>: record the work items of step KPM_TRACE_STEP (default 2)
+    const char *trace_path = getenv("KPM_TRACE");
+    const int trace_step = getenv("KPM_TRACE_STEP") ? atoi(getenv("KPM_TRACE_STEP")) : 2;
+    const int64_t trace_items = r->g->n_chunks + p.n_heavy_tasks;
+    if (trace_path && r->done_steps == trace_step && trace_items > 0)
+      KPM_CUDA(cudaMallocAsync(&p.trace, sizeof(unsigned long long) * 3 * trace_items, st));
     KPM_CUDA(launch_step(r, p, false, first, st));
+    if (p.trace) {
+      std::vector<unsigned long long> tr(3 * trace_items);
+      KPM_CUDA(cudaMemcpyAsync(tr.data(), p.trace, sizeof(unsigned long long) * tr.size(),
+                               cudaMemcpyDeviceToHost, st));
+      KPM_CUDA(cudaStreamSynchronize(st));
+      KPM_CUDA(cudaFreeAsync(p.trace, st));
+      if (FILE *fp = fopen(trace_path, "wb")) {
+        const long long hdr[4] = {(long long)p.n_heavy_tasks, (long long)r->g->n_chunks,
+                                  (long long)r->ld, (long long)r->g->n_heavy};
+        fwrite(hdr, sizeof(hdr), 1, fp);
+        fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fp);
+        std::vector<int32_t> cs(r->g->n_chunks + 1), co(r->g->n_chunks);
+        std::vector<int64_t> rp(r->g->n + 1);
+        cudaMemcpy(cs.data(), r->g->chunk_start, sizeof(int32_t) * cs.size(), cudaMemcpyDeviceToHost);
+        cudaMemcpy(co.data(), r->g->chunk_order, sizeof(int32_t) * co.size(), cudaMemcpyDeviceToHost);
+        cudaMemcpy(rp.data(), r->g->row_ptr, sizeof(int64_t) * rp.size(), cudaMemcpyDeviceToHost);
+        // per chunk id: rows, nonzeros, empty rows
+        std::vector<int64_t> cst(3 * (size_t)r->g->n_chunks);
+        for (int32_t c = 0; c < r->g->n_chunks; ++c) {
+          int64_t empty = 0;
+          for (int32_t i = cs[c]; i < cs[c + 1]; ++i) empty += rp[i + 1] == rp[i];
+          cst[3 * c] = cs[c + 1] - cs[c];
+          cst[3 * c + 1] = rp[cs[c + 1]] - rp[cs[c]];
+          cst[3 * c + 2] = empty;
+        }
+        fwrite(co.data(), sizeof(int32_t), co.size(), fp);
+        fwrite(cst.data(), sizeof(int64_t), cst.size(), fp);
+        fclose(fp);
+      }
+    }
     if (r->timing) KPM_CUDA(cudaEventRecord(r->ev[2 * r->ev_used++ + 1], st));
     const int m = r->k_index + 1;
     if (r->mode == KPM_MODE_LDOS && r->g->n_heavy > 0) {
