@@ -54,6 +54,28 @@ CONFIGS = {
 METRIC = "KPM nnz*probes*moments/sec (G/s) and achieved HBM GB/s"
 
 
+def _tiled(P):
+    """kpm_step.cu launch_c: P > 64 probes (4-column layout, ld % 4 == 0) run
+    as 64-column TMA gather4 passes unless KPM_TILE=0 / KPM_G4=0."""
+    ld = -(-P // 4) * 4
+    return (P > 64 and ld % 4 == 0 and os.environ.get("KPM_TILE", "1") != "0"
+            and os.environ.get("KPM_G4", "1") != "0")
+
+
+def _step_launches(P):
+    return -(-P // 64) if _tiled(P) else 1
+
+
+def _kernel_label(P):
+    if _tiled(P):
+        return "kpm_step_g4_kernel<C=2,DBL> x%d column tiles (TMA gather4)" % _step_launches(P)
+    if P <= 64 and os.environ.get("KPM_G4", "1") != "0":
+        return "kpm_step_g4_kernel<DBL> (TMA gather4)"
+    if os.environ.get("KPM_BULK", "2") != "0":
+        return "kpm_step_bulk_kernel<DBL> (TMA bulk-copy gathers)"
+    return "kpm_step_kernel<DBL>"
+
+
 def _peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -280,9 +302,7 @@ def run_ours(args):
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "bytes_per_launch_model": bstep,
                          "bytes_per_launch_compulsory": _compulsory_bytes(n, nnz, P),
-                         "kernel": ("kpm_step_bulk_kernel<DBL> (TMA bulk-copy gathers)"
-                                    if os.environ.get("KPM_BULK", "2") != "0"
-                                    else "kpm_step_kernel<DBL>"),
+                         "kernel": _kernel_label(P),
                          "kernel_ms": round(kern_avg, 4),
                          "hbm_gbs_model_per_step": round(bstep / (ms_step * 1e-3) / 1e9, 1),
                          # measured DRAM bytes per launch (ncu, profiles/traffic.json)
@@ -292,7 +312,9 @@ def run_ours(args):
                          "traffic_frac": (round(traffic / (kern_avg * 1e-3) / 1e9 / peak, 4)
                                           if traffic else None)},
             "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": 2 * args.steps,
+            # per step: the step kernel (one launch per 64-column tile) +
+            # reduce_groups + finalize
+            "gpu_launches": (_step_launches(P) + 2) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

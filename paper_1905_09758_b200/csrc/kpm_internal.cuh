@@ -128,6 +128,6 @@ struct kpm_run {
   int32_t ev_used = 0;
   // TMA tensor maps of the two recurrence blocks (n x ld fp64, box ld x 1) for
   // the gather4 light path (kpm_step.cu light_g4); tm_ok when encodable
-  CUtensorMap tm[2];
-  bool tm_ok = false;
+  CUtensorMap tm[2][3];  // [block][box: whole row, 64-column tile, last partial tile]
+  bool tm_ok = false, tm_tile_ok = false;
 };

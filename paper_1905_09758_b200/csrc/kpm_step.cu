@@ -76,6 +76,8 @@ struct StepParams {
   double hot_dinv;         // gathered rows with dinv_j <= hot_dinv are "hot" (L2 policy)
   int bulk;                // TMA bulk-copy gathers (light_bulk): 0 off, 1 C=4, 2 all
   double *hldos;           // n_heavy x n_slices (LDOS)
+  int64_t col0, tw;        // column tile of this launch: [col0, col0 + tw) (default 0, ld)
+  int tile;                // run the 4-column layout as 64-column gather4 tiles
   int g4;                  // TMA gather4 light path: 0 off, 1 for C <= 2, 2 all layouts
   int lean;                // per-lane async gathers for C <= 2 (light_lean)
   int64_t hub_off;         // dynamic smem (doubles) of warp 0's hub ring (kpm_step_kernel)
@@ -150,15 +152,15 @@ __device__ __forceinline__ void heavy_task(const StepParams &p, int64_t t, doubl
   const int lane = threadIdx.x & 31;
   const int nb = lane >> 2, cg = lane & 3;
   const int64_t ld = p.ld;
-  const int nsl = (int)((ld + kSlice - 1) / kSlice);
+  const int nsl = (int)((p.tw + kSlice - 1) / kSlice);  // slices of this launch's column tile
   const int h = (int)(t / nsl), sl = (int)(t % nsl);
   const int i = p.heavy_rows[h];
   const int64_t beg = p.row_ptr[i], end = p.row_ptr[i + 1];
   const int64_t d = end - beg;
   double di = 0.0;
   if constexpr (!EXPL) di = p.dinv[p.row0 + i];
-  const int64_t c = (int64_t)sl * kSlice + cg;
-  const bool active = c < ld;
+  const int64_t c = p.col0 + (int64_t)sl * kSlice + cg;
+  const bool active = (int64_t)sl * kSlice + cg < p.tw;
   const uint32_t rows_sa = smem_u32(hub);                     // [D][32] doubles
   const uint32_t w_sa = rows_sa + kHubDepth * 32 * 8;         // [D][8] doubles
   const uint32_t col_sa = w_sa + kHubDepth * 8 * 8;           // [2D][8] int32
@@ -1400,14 +1402,24 @@ __global__ void __launch_bounds__(256, KPM_LEAN_MINB) kpm_step_lean_kernel(const
 // wave also has the col ids of the wave its slot is refilled with.  The
 // consumer adds the rows IN CSR ORDER from shared memory (bit-identical sums);
 // own operands come through the light_lean prefetch ring.
+// Tuning (B200 sweep, profiles/r01_ncu_summary.md): 24 warps per SM with 4 KB
+// of rows per warp beat 16 warps with 8 KB (P=32 26.1 -> 23.5 ms, P=64 38.5 ->
+// 32.3 ms on C3): the light path is bound by dependent-instruction latency
+// more than by bytes in flight, so warps beat ring depth; 32 warps spill.
 #ifndef KPM_G4_WAVE1
 #define KPM_G4_WAVE1 16
+#endif
+#ifndef KPM_G4_ROWKB
+#define KPM_G4_ROWKB 4
+#endif
+#ifndef KPM_G4_OWN
+#define KPM_G4_OWN 4
 #endif
 template <int C, int MODE, bool EXPL, bool FIRST>
 struct G4 {
   static constexpr int WAVE = C == 1 ? KPM_G4_WAVE1 : (C == 2 ? 8 : 4);  // neighbours per wave
-  static constexpr int D = 32 / (WAVE * C);  // waves in flight: 8 KB of rows
-  static constexpr int R = C == 4 ? 2 : 8 / C;  // own-row prefetch depth
+  static constexpr int D = KPM_G4_ROWKB * 4 / (WAVE * C);  // waves in flight (KB of rows)
+  static constexpr int R = C == 4 ? 2 : KPM_G4_OWN / C;  // own-row prefetch depth
   static constexpr int NOP = Lean<C, MODE, EXPL, FIRST>::NOP;
   static constexpr int W = 32 * C;
   static constexpr int slot_d = ((WAVE * W * 8 + 127) / 128) * 128 / 8;  // one wave's rows
@@ -1418,14 +1430,15 @@ struct G4 {
   static constexpr int bar_d = D + R;
   static constexpr int data_d = rows_d + wv_d + col_d + own_d;
   static constexpr int warp_d = ((data_d > kHubRingDoubles ? data_d : kHubRingDoubles) + bar_d + 15) / 16 * 16;
+  static_assert(D >= 1 && R >= 1 && (R & (R - 1)) == 0, "gather4 ring shape");
 };
 
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm, int j0, int j1,
-                                            int j2, int j3, uint32_t bar) {
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm, int x, int j0,
+                                            int j1, int j2, int j3, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-      "l"(tm), "r"(0), "r"(j0), "r"(j1), "r"(j2), "r"(j3), "r"(bar)
+      "l"(tm), "r"(x), "r"(j0), "r"(j1), "r"(j2), "r"(j3), "r"(bar)
       : "memory");
 }
 
@@ -1436,8 +1449,9 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
   constexpr int D = L::D, R = L::R, W = L::W, NOP = L::NOP, WAVE = L::WAVE;
   const int lane = threadIdx.x & 31;
   const int64_t ld = p.ld;
-  const int64_t c0 = (int64_t)lane * C;
-  const bool active = c0 < ld;
+  // this launch's column tile [col0, col0 + tw): lane l owns columns col0 + [lC, lC + C)
+  const int64_t c0 = p.col0 + (int64_t)lane * C;
+  const bool active = (int64_t)lane * C < p.tw;
   const int r0 = p.chunk_start[chunk], r1 = p.chunk_start[chunk + 1];
   double s1[C], s2[C];
 #pragma unroll
@@ -1456,7 +1470,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
   const uint32_t own_sa = col_sa + L::col_d * 8;
   uint64_t *wbar = reinterpret_cast<uint64_t *>(base + L::warp_d - L::bar_d);
   uint64_t *obar = wbar + D;
-  const uint32_t rbytes = (uint32_t)ld * 8u;
+  const uint32_t rbytes = (uint32_t)p.tw * 8u;  // one gathered row segment in shared memory
 
   int wb = r0;
   int64_t wrp = p.row_ptr[min(r0 + lane, r1)];
@@ -1516,7 +1530,8 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       const uint32_t dst = rows_sa + sl * (uint32_t)(L::slot_d * 8);
 #pragma unroll
       for (int q = 0; q < WAVE / 4; ++q)
-        tma_gather4(dst + 4 * q * rbytes, tm, j[4 * q], j[4 * q + 1], j[4 * q + 2], j[4 * q + 3], bar);
+        tma_gather4(dst + 4 * q * rbytes, tm, (int)p.col0, j[4 * q], j[4 * q + 1], j[4 * q + 2],
+                    j[4 * q + 3], bar);
     }
     if (lane < cnt) {
       const uint32_t wd = wv_sa + (sl * WAVE + lane) * 8;
@@ -1589,7 +1604,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
   };
   advance(0);
 
-  const uint32_t my_col = (uint32_t)(active ? c0 : 0) * 8u;
+  const uint32_t my_col = (uint32_t)(active ? lane * C : 0) * 8u;
   for (int w = 0; w < nw; ++w) {
     const uint32_t sl = (uint32_t)(w % D);
     mbar_wait(wbar + sl, (wphase >> sl) & 1u);
@@ -1636,7 +1651,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
 }
 
 #ifndef KPM_G4_MINB
-#define KPM_G4_MINB 2
+#define KPM_G4_MINB 3
 #endif
 template <int C, int MODE, bool EXPL, bool FIRST>
 __global__ void __launch_bounds__(256, KPM_G4_MINB)
@@ -1916,8 +1931,7 @@ static cudaError_t launch_g4_k(const kpm_run *r, const StepParams &p, const CUte
 
 template <int C, int MODE>
 static cudaError_t launch_g4(const kpm_run *r, const StepParams &p, bool expl, bool first,
-                             cudaStream_t st) {
-  const CUtensorMap &tm = r->tm[p.X == r->a ? 0 : 1];
+                             const CUtensorMap &tm, cudaStream_t st) {
   if (expl && first) return launch_g4_k<C, MODE, true, true>(r, p, tm, st);
   if (expl) return launch_g4_k<C, MODE, true, false>(r, p, tm, st);
   if (first) return launch_g4_k<C, MODE, false, true>(r, p, tm, st);
@@ -1937,10 +1951,26 @@ template <int C, int MODE, bool INIT>
 static cudaError_t launch_c(const kpm_run *r, const StepParams &p, bool expl, bool first,
                             cudaStream_t st) {
   if constexpr (!INIT) {
+    const int blk = p.X == r->a ? 0 : (p.X == r->b ? 1 : -1);
+    // the 4-column layout of the global modes as 64-column gather4 passes over
+    // the same row-major blocks: smaller gathered segments keep twice the rows
+    // in L2 and run 24 warps per SM (C3: 2 x 32.2 ms vs 70.0 ms per step);
+    // every column's sums are unchanged, so the results are bitwise the same
+    if (C == 4 && MODE != MODE_LDOS && p.tile && p.g4 && r->tm_tile_ok && p.nparts <= 1 &&
+        blk >= 0) {
+      for (int64_t t0 = 0; t0 < p.ld; t0 += 64) {
+        StepParams q = p;
+        q.col0 = t0;
+        q.tw = p.ld - t0 < 64 ? p.ld - t0 : 64;
+        q.n_heavy_tasks = (int64_t)p.n_heavy * ((q.tw + kSlice - 1) / kSlice);
+        cudaError_t e = launch_g4<2, MODE>(r, q, expl, first, r->tm[blk][q.tw == 64 ? 1 : 2], st);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    }
     // TMA gather4 for one column tile (tensor maps of both blocks encoded)
-    if (p.ld <= 32 * C && p.g4 >= (C == 4 ? 2 : 1) && r->tm_ok && p.nparts <= 1 &&
-        (p.X == r->a || p.X == r->b))
-      return launch_g4<C, MODE>(r, p, expl, first, st);
+    if (p.ld <= 32 * C && p.g4 >= (C == 4 ? 2 : 1) && r->tm_ok && p.nparts <= 1 && blk >= 0)
+      return launch_g4<C, MODE>(r, p, expl, first, r->tm[blk][0], st);
   }
   if constexpr (!INIT && C <= 2) {
     // per-lane async gathers for one column tile of 1 or 2 columns per lane
@@ -2044,6 +2074,10 @@ static StepParams base_params(const kpm_run *r) {
   p.hldos = r->hldos;
   p.stream = 1;
   if (const char *e = getenv("KPM_STREAM")) p.stream = atoi(e);
+  p.col0 = 0;
+  p.tw = r->ld;
+  p.tile = 1;  // 4-column layouts (DOS modes) as 64-column gather4 passes (KPM_TILE=0: off)
+  if (const char *e = getenv("KPM_TILE")) p.tile = atoi(e);
   p.g4 = 1;  // TMA gather4 light path for the 1- and 2-column layouts (KPM_G4=2: also 4)
   if (const char *e = getenv("KPM_G4")) p.g4 = atoi(e);
   p.lean = 1;  // per-lane async gathers for the 1- and 2-column layouts (KPM_LEAN=0: off)
@@ -2242,15 +2276,24 @@ static void encode_block_maps(kpm_run *r) {
   if (!enc) return;
   const cuuint64_t dims[2] = {(cuuint64_t)r->ld, (cuuint64_t)g->n};
   const cuuint64_t strides[1] = {(cuuint64_t)r->ld * sizeof(double)};
-  const cuuint32_t box[2] = {(cuuint32_t)r->ld, 1};
   const cuuint32_t es[2] = {1, 1};
   double *blk[2] = {r->a, r->b};
-  for (int q = 0; q < 2; ++q)
-    if (enc(&r->tm[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, blk[q], dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return;
-  r->tm_ok = true;
+  // box widths: [0] the whole row, [1] a 64-column tile, [2] the last partial tile
+  const cuuint32_t widths[3] = {(cuuint32_t)r->ld, 64, (cuuint32_t)(r->ld % 64)};
+  auto encode = [&](int q, int kind) {
+    const cuuint32_t box[2] = {widths[kind], 1};
+    return enc(&r->tm[q][kind], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, blk[q], dims, strides, box,
+               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  bool ok = true, tile_ok = r->ld > 64;
+  for (int q = 0; q < 2; ++q) {
+    ok = ok && encode(q, 0);
+    if (tile_ok) tile_ok = encode(q, 1) && (widths[2] == 0 || encode(q, 2));
+  }
+  r->tm_ok = ok;
+  r->tm_tile_ok = ok && tile_ok;
 }
 
 extern "C" {

@@ -493,3 +493,52 @@ def test_filtered_probes_stay_on_device(golden, kpm_ctx):
     assert np.array_equal(fd.columns, fh.columns)
     half = fd.column_slice(4, 12)
     assert np.array_equal(half.columns, fh.columns[:, 4:12])
+
+
+# Every light-row gather path of the step kernel, selected by environment
+# (kpm_step.cu launch_c): TMA gather4 (default for ld % 4 == 0; the 4-column
+# layout of the global modes as 64-column tiles, or whole rows with KPM_G4=2
+# KPM_TILE=0), per-lane cp.async (KPM_G4=0), TMA bulk copies
+# (KPM_LEAN=0) and register gathers (KPM_BULK=0); each with and without forced
+# hub rows (cp.async hub pipeline), on the implicit normalized adjacency and on
+# explicit values with shift/scale.  T blocks must be bit-identical to the
+# oracle's restated recurrence (the reference's _row order, no FMA).
+_PATHS = {
+    "tiles": {},  # default: gather4, 4-column layouts as 64-column passes
+    "g4": {"KPM_G4": "2", "KPM_TILE": "0"},
+    "lean": {"KPM_G4": "0"},
+    "bulk": {"KPM_G4": "0", "KPM_LEAN": "0"},
+    "register": {"KPM_G4": "0", "KPM_LEAN": "0", "KPM_BULK": "0"},
+}
+
+
+@pytest.mark.parametrize("path", sorted(_PATHS))
+@pytest.mark.parametrize("P", [4, 20, 30, 32, 36, 64, 100, 128])
+@pytest.mark.parametrize("hubs", [False, True])
+def test_light_paths_bitexact(oracle, kpm_ctx, monkeypatch, path, P, hubs):
+    for k in ("KPM_G4", "KPM_TILE", "KPM_LEAN", "KPM_BULK", "KPM_HEAVY_DEGREE"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in _PATHS[path].items():
+        monkeypatch.setenv(k, v)
+    if hubs:
+        monkeypatch.setenv("KPM_HEAVY_DEGREE", "40")
+    g = kp.preferential_attachment(3000, 3, seed=P)
+    # 70 isolated vertices inserted at id 1500 and 30 appended: runs of empty rows
+    ins = lambda v: v + 70 * (v >= 1500)
+    deg = np.diff(g.row_ptr)
+    deg = np.concatenate([deg[:1500], np.zeros(70, np.int64), deg[1500:], np.zeros(30, np.int64)])
+    n = g.n + 100
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    ci = ins(g.col_idx.astype(np.int64))
+    z = oracle.make_probes(n, P, "rademacher", seed=P + 1)
+    dinv = oracle.dinv_of(rp)
+    for mode in (_lib.MODE_DOS_DOUBLING, _lib.MODE_DOS_DIRECT, _lib.MODE_LDOS):
+        dev = kp.DeviceGraph.from_csr(n, rp, ci)
+        want = oracle.c_recurrence_block(rp, ci, oracle.normadj_values(rp, ci, dinv), z, 5,
+                                         threads=8)
+        assert np.array_equal(_block_after(dev, z, mode, 5, kpm_ctx), want), (path, mode)
+    # explicit values (a shifted/scaled Laplacian-like operator)
+    vals = -oracle.normadj_values(rp, ci, dinv)
+    dev = kp.DeviceGraph.from_csr(n, rp, ci, values=vals, shift=0.25, scale=1.5)
+    want = oracle.c_recurrence_block(rp, ci, vals, z, 5, shift=0.25, scale=1.5, threads=8)
+    assert np.array_equal(_block_after(dev, z, _lib.MODE_DOS_DIRECT, 5, kpm_ctx), want), path
