@@ -305,7 +305,7 @@ def run_ours(args):
                          "kernel": _kernel_label(P),
                          "kernel_ms": round(kern_avg, 4),
                          "hbm_gbs_model_per_step": round(bstep / (ms_step * 1e-3) / 1e9, 1),
-                         # measured DRAM bytes per launch (ncu, profiles/traffic.json)
+                         # measured DRAM bytes per step (ncu, profiles/traffic.json; all tile launches)
                          # over the live kernel time: the DRAM-side fraction
                          "traffic_GBs": (round(traffic / (kern_avg * 1e-3) / 1e9, 1)
                                          if traffic else None),

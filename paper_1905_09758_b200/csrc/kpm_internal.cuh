@@ -59,6 +59,7 @@ int stage_in(cudaStream_t s, const void *p, size_t bytes, DevBuf &tmp,
 struct kpm_ctx {
   int device = 0;
   int sm_count = 148;
+  size_t persist_max = 0;  // cudaDeviceProp::persistingL2CacheMaxSize
   cudaStream_t stream = nullptr;
 };
 

@@ -80,6 +80,7 @@ struct StepParams {
   int tile;                // run the 4-column layout as 64-column gather4 tiles
   int g4;                  // TMA gather4 light path: 0 off, 1 for C <= 2, 2 all layouts
   int lean;                // per-lane async gathers for C <= 2 (light_lean)
+  int g4hint;              // gather4 L2 hint experiment: 0 none, 1 evict_last, 2 evict_first
   int64_t hub_off;         // dynamic smem (doubles) of warp 0's hub ring (kpm_step_kernel)
   unsigned long long *trace;  // KPM_TRACE: per work item (start ns, end ns, smid<<32|warp)
 };
@@ -1433,6 +1434,16 @@ struct G4 {
   static_assert(D >= 1 && R >= 1 && (R & (R - 1)) == 0, "gather4 ring shape");
 };
 
+__device__ __forceinline__ void tma_gather4_hint(uint32_t dst, const CUtensorMap *tm, int x,
+                                                 int j0, int j1, int j2, int j3, uint32_t bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+      "l"(tm), "r"(x), "r"(j0), "r"(j1), "r"(j2), "r"(j3), "r"(bar), "l"(pol)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm, int x, int j0,
                                             int j1, int j2, int j3, uint32_t bar) {
   asm volatile(
@@ -1528,10 +1539,22 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
                    "r"((uint32_t)WAVE * rbytes)
                    : "memory");
       const uint32_t dst = rows_sa + sl * (uint32_t)(L::slot_d * 8);
+      if (p.g4hint) {
+        uint64_t pol;
+        if (p.g4hint == 1)
+          asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        else
+          asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll
-      for (int q = 0; q < WAVE / 4; ++q)
-        tma_gather4(dst + 4 * q * rbytes, tm, (int)p.col0, j[4 * q], j[4 * q + 1], j[4 * q + 2],
-                    j[4 * q + 3], bar);
+        for (int q = 0; q < WAVE / 4; ++q)
+          tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)p.col0, j[4 * q], j[4 * q + 1],
+                           j[4 * q + 2], j[4 * q + 3], bar, pol);
+      } else {
+#pragma unroll
+        for (int q = 0; q < WAVE / 4; ++q)
+          tma_gather4(dst + 4 * q * rbytes, tm, (int)p.col0, j[4 * q], j[4 * q + 1], j[4 * q + 2],
+                      j[4 * q + 3], bar);
+      }
     }
     if (lane < cnt) {
       const uint32_t wd = wv_sa + (sl * WAVE + lane) * 8;
@@ -2082,6 +2105,8 @@ static StepParams base_params(const kpm_run *r) {
   if (const char *e = getenv("KPM_G4")) p.g4 = atoi(e);
   p.lean = 1;  // per-lane async gathers for the 1- and 2-column layouts (KPM_LEAN=0: off)
   if (const char *e = getenv("KPM_LEAN")) p.lean = atoi(e);
+  p.g4hint = 0;
+  if (const char *e = getenv("KPM_G4_HINT")) p.g4hint = atoi(e);
   p.bulk = 2;  // bulk-copy gathers in every layout (KPM_BULK=1: 4-column only, 0: none)
   if (const char *e = getenv("KPM_BULK")) p.bulk = atoi(e);
   // hot rows (L2 evict_last in the bulk path): the highest-degree rows whose
@@ -2089,7 +2114,8 @@ static StepParams base_params(const kpm_run *r) {
   // KPM_HOT_DEGREE=<d> overrides (0 disables)
   p.hot_dinv = -1.0;
   {
-    constexpr double kHotBytes = 64.0 * 1024 * 1024;
+    double kHotBytes = 64.0 * 1024 * 1024;
+    if (const char *e = getenv("KPM_HOT_MB")) kHotBytes = atof(e) * 1024 * 1024;
     const double budget = kHotBytes / (8.0 * (double)r->ld);
     double rows = 0.0, hot_deg = 0.0;
     for (int b = 63; b >= 0; --b) {
