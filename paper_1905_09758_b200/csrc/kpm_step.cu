@@ -1403,23 +1403,45 @@ __global__ void __launch_bounds__(256, KPM_LEAN_MINB) kpm_step_lean_kernel(const
 // wave also has the col ids of the wave its slot is refilled with.  The
 // consumer adds the rows IN CSR ORDER from shared memory (bit-identical sums);
 // own operands come through the light_lean prefetch ring.
-// Tuning (B200 sweep, profiles/r01_ncu_summary.md): 24 warps per SM with 4 KB
-// of rows per warp beat 16 warps with 8 KB (P=32 26.1 -> 23.5 ms, P=64 38.5 ->
-// 32.3 ms on C3): the light path is bound by dependent-instruction latency
-// more than by bytes in flight, so warps beat ring depth; 32 warps spill.
+// Tuning (B200 sweeps, profiles/r01_ncu_summary.md): one wave in flight per
+// warp.  Session 2: 24 warps per SM with 4 KB of rows per warp beat 16 warps
+// with 8 KB in two 8-row waves (P=32 26.1 -> 23.5 ms, P=64 38.5 -> 32.3 ms on
+// C3).  Session 3: the per-wave bookkeeping (issue, barrier, row-end checks:
+// ~140 of the ~210 instructions per 8-row wave) costs power under the B200's
+// power cap, so for P=64 one 16-row wave per warp at 16 warps per SM wins in
+// the steady state (C3 P=128 as two 64-column tiles 73.1 -> 69.2 ms), and for
+// P=32 one 32-row wave at 16 warps per SM (C3 24.9 -> 23.2 ms, C5 neutral).
 #ifndef KPM_G4_WAVE1
-#define KPM_G4_WAVE1 16
+#define KPM_G4_WAVE1 32
 #endif
-#ifndef KPM_G4_ROWKB
-#define KPM_G4_ROWKB 4
+#ifndef KPM_G4_D1
+#define KPM_G4_D1 1
+#endif
+#ifndef KPM_G4_MINB1
+#define KPM_G4_MINB1 2
+#endif
+#ifndef KPM_G4_WAVE2
+#define KPM_G4_WAVE2 16
+#endif
+#ifndef KPM_G4_D2
+#define KPM_G4_D2 1
+#endif
+#ifndef KPM_G4_MINB2
+#define KPM_G4_MINB2 2
 #endif
 #ifndef KPM_G4_OWN
 #define KPM_G4_OWN 4
 #endif
+template <int C>
+struct G4Tune {  // neighbours per wave, waves in flight, resident 256-thread CTAs
+  static constexpr int wave = C == 1 ? KPM_G4_WAVE1 : (C == 2 ? KPM_G4_WAVE2 : 4);
+  static constexpr int d = C == 1 ? KPM_G4_D1 : (C == 2 ? KPM_G4_D2 : 1);
+  static constexpr int minb = C == 1 ? KPM_G4_MINB1 : (C == 2 ? KPM_G4_MINB2 : 3);
+};
 template <int C, int MODE, bool EXPL, bool FIRST>
 struct G4 {
-  static constexpr int WAVE = C == 1 ? KPM_G4_WAVE1 : (C == 2 ? 8 : 4);  // neighbours per wave
-  static constexpr int D = KPM_G4_ROWKB * 4 / (WAVE * C);  // waves in flight (KB of rows)
+  static constexpr int WAVE = G4Tune<C>::wave;  // neighbours per wave
+  static constexpr int D = G4Tune<C>::d;        // waves in flight
   static constexpr int R = C == 4 ? 2 : KPM_G4_OWN / C;  // own-row prefetch depth
   static constexpr int NOP = Lean<C, MODE, EXPL, FIRST>::NOP;
   static constexpr int W = 32 * C;
@@ -1673,11 +1695,8 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
   }
 }
 
-#ifndef KPM_G4_MINB
-#define KPM_G4_MINB 3
-#endif
 template <int C, int MODE, bool EXPL, bool FIRST>
-__global__ void __launch_bounds__(256, KPM_G4_MINB)
+__global__ void __launch_bounds__(256, G4Tune<C>::minb)
 kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
   using L = G4<C, MODE, EXPL, FIRST>;
   extern __shared__ __align__(128) double sg4[];

@@ -427,22 +427,57 @@ class MotifSet(list):
 
 def _scan_classes(rows, head, ok):
     """Classes from a device signature scan: runs of equal signature whose
-    members all matched the run head exactly; runs holding a mismatch (hash
-    collision) come back as a list of row arrays for exact regrouping."""
+    members all matched the run head exactly, as (ptr, members) CSR arrays
+    ordered by smallest member (rows of a run are ascending: the device sort
+    is stable over row order); runs holding a mismatch (hash collision) come
+    back as a list of row arrays for exact regrouping."""
     n = rows.shape[0]
     if n == 0:
-        return [], []
+        return np.zeros(1, np.int64), np.zeros(0, np.int64), []
     starts = np.flatnonzero(head == np.arange(n))
     lens = np.diff(np.append(starts, n))
     head_ok = ok[starts].astype(bool)
-    run_of = np.repeat(np.arange(starts.size), lens)
-    bad = np.zeros(starts.size, dtype=bool)
-    np.logical_or.at(bad, run_of, ok == 0)
+    bad = np.logical_or.reduceat(ok == 0, starts)
     keep = head_ok & ~bad & (lens >= 2)
     collide = head_ok & bad
-    classes = [rows[s:s + l] for s, l in zip(starts[keep].tolist(), lens[keep].tolist())]
     fallback = [rows[s:s + l] for s, l in zip(starts[collide].tolist(), lens[collide].tolist())]
-    return classes, fallback
+    ks, kl = starts[keep], lens[keep]
+    order = np.argsort(rows[ks], kind="stable")
+    ks, kl = ks[order], kl[order]
+    ptr = np.zeros(ks.size + 1, np.int64)
+    np.cumsum(kl, out=ptr[1:])
+    members = rows[np.repeat(ks - ptr[:-1], kl) + np.arange(ptr[-1])]
+    return ptr, members, fallback
+
+
+def _merge_classes(ptr, members, extra):
+    """(ptr, members) plus extra class arrays, re-ordered by smallest member."""
+    if not extra:
+        return ptr, members
+    classes = [members[a:b] for a, b in zip(ptr[:-1].tolist(), ptr[1:].tolist())] + extra
+    classes.sort(key=lambda c: int(c[0]))
+    sizes = np.fromiter((c.size for c in classes), np.int64, len(classes))
+    ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    return ptr, np.concatenate(classes).astype(np.int64)
+
+
+def _instances(kind, ptr, members, eig, details, operator):
+    """MotifInstance objects for detected classes without the per-object
+    conversions of __init__ (kind, nodes and values are already canonical)."""
+    ml, pl = members.tolist(), ptr.tolist()
+    new = object.__new__
+    out = []
+    append = out.append
+    for i, (lam, det) in enumerate(zip(eig, details)):
+        inst = new(MotifInstance)
+        inst.kind = kind
+        inst.nodes = tuple(ml[pl[i]:pl[i + 1]])
+        inst.eigenvalue = lam
+        inst._eigvecs = None
+        inst.detail = det
+        inst._operator = operator
+        append(inst)
+    return out
 
 
 def _detect_device(g, kinds, operator) -> "MotifSet":
@@ -492,27 +527,23 @@ def _detect_device(g, kinds, operator) -> "MotifSet":
         if kind not in kinds:
             arrays[kind] = (np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
             continue
-        classes, fallback = _scan_classes(rows, head, ok)
-        classes += _exact(fallback, closed)
-        classes.sort(key=lambda c: int(c[0]))
-        sizes = np.fromiter((c.size for c in classes), np.int64, len(classes))
-        ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-        members = np.concatenate(classes) if classes else np.zeros(0, np.int64)
-        arrays[kind] = (ptr, members, deg[members[ptr[:-1]]] if classes else np.zeros(0))
+        ptr, members, fallback = _scan_classes(rows, head, ok)
+        ptr, members = _merge_classes(ptr, members, _exact(fallback, closed))
+        cdeg = deg[members[ptr[:-1]]]
+        arrays[kind] = (ptr, members, cdeg)
+        dl = cdeg.tolist()
         if closed:
-            for c in classes:
-                d = float(deg[c[0]])
-                inst = MotifInstance(kind, tuple(c.tolist()), 0.0,
-                                     detail={"degree": d, "weight": 1.0}, operator=operator)
-                inst.eigenvalue = float(_twin_modes(operator, kind, d, 1.0))
-                items.append(inst)
+            if cdeg.size and cdeg.min() <= 0:
+                raise MotifError("closed twins require positive degree")
+            eig = [float(_twin_modes(operator, kind, d, 1.0)) for d in dl] \
+                if operator is not OperatorKind.NORMALIZED_ADJACENCY else (-1.0 / cdeg).tolist()
+            details = [{"degree": d, "weight": 1.0} for d in dl]
         else:
-            for c in classes:
-                d = float(deg[c[0]])
-                inst = MotifInstance(kind, tuple(c.tolist()), 0.0, detail={"degree": d},
-                                     operator=operator)
-                inst.eigenvalue = float(_twin_modes(operator, kind, d, 1.0))
-                items.append(inst)
+            eig = [float(_twin_modes(operator, kind, d, 1.0)) for d in dl] \
+                if operator is OperatorKind.LAPLACIAN else \
+                [float(_twin_modes(operator, kind, 1.0, 1.0))] * len(dl)
+            details = [{"degree": d} for d in dl]
+        items.extend(_instances(kind, ptr, members, eig, details, operator))
     if MotifKind.DANGLING_TWO_CHAIN in kinds:
         xs = np.flatnonzero(hub >= 0)
         order = np.argsort(hub[xs], kind="stable")

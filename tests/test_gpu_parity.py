@@ -462,12 +462,16 @@ def test_device_motif_scan_matches_reference(golden, golden_meta, kpm_ctx):
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3])
-def test_device_motif_scan_matches_host(kpm_ctx, seed):
+@pytest.mark.parametrize("operator", ["normalized-adjacency", "adjacency", "laplacian",
+                                      "normalized-laplacian"])
+def test_device_motif_scan_matches_host(kpm_ctx, seed, operator):
     g = kp.testkit.motif_heavy(n_ba=4000, m=2, seed=seed, twin_pairs=300, stars=80)
     for kinds in (None, {kp.MotifKind.CLOSED_TWIN}, {kp.MotifKind.DANGLING_TWO_CHAIN}):
-        dev = kp.detect_motifs(g, kinds=kinds)
-        host = kp.detect_motifs(g, kinds=kinds, device=False)
+        dev = kp.detect_motifs(g, kinds=kinds, operator=operator)
+        host = kp.detect_motifs(g, kinds=kinds, operator=operator, device=False)
         assert [_inst_key(i) for i in dev] == [_inst_key(i) for i in host]
+        assert [(repr(i.detail), i._operator) for i in dev] == \
+            [(repr(i.detail), i._operator) for i in host]
     # isolated nodes form one open-twin class; loops are excluded
     g2 = kp.build_csr([(0, 1), (0, 2), (3, 3), (4, 5)], n=9, allow_self_loops=True)
     assert [_inst_key(i) for i in kp.detect_motifs(g2)] == \

@@ -283,3 +283,40 @@ def test_lazy_instances_match_reference_fields(golden_meta, golden):
     for got, w in zip(insts, golden_meta["motif"]["instances"]):
         assert got.multiplicity == w[3]
         assert len(got.eigvecs) == w[3]
+
+
+def test_device_scan_extraction_host_logic():
+    """motifs._scan_classes / _merge_classes / _instances (the host half of
+    device detection): runs of a stable (hash, row) sort become classes ordered
+    by smallest member; runs with a failed exact check go to the collision
+    fallback; heads that failed are dropped; singletons are not classes."""
+    rng = np.random.default_rng(7)
+    n_runs = 500
+    runs = [np.sort(rng.choice(10_000, rng.integers(1, 5), replace=False)) for _ in range(n_runs)]
+    collide_run, dead_run = 3, 4
+    runs[collide_run] = np.array([1, 2, 3]) + 20_000
+    runs[dead_run] = np.array([4, 5]) + 20_000
+    rows = np.concatenate(runs).astype(np.int64)
+    starts = np.cumsum([0] + [r.size for r in runs[:-1]])
+    head = np.repeat(starts, [r.size for r in runs]).astype(np.int64)
+    ok = np.ones(rows.size, np.int8)
+    ok[starts[collide_run] + 1] = 0
+    ok[starts[dead_run]] = 0
+    ptr, members, fallback = M._scan_classes(rows, head, ok)
+    assert len(fallback) == 1 and np.array_equal(fallback[0], runs[collide_run])
+    want = sorted((r for i, r in enumerate(runs) if r.size >= 2 and i not in (collide_run, dead_run)),
+                  key=lambda r: int(r[0]))
+    got = [members[a:b] for a, b in zip(ptr[:-1], ptr[1:])]
+    assert len(got) == len(want) and all(np.array_equal(a, b) for a, b in zip(got, want))
+    extra = [np.array([20_001, 20_003])]
+    ptr2, mem2 = M._merge_classes(ptr, members, extra)
+    want2 = sorted(want + extra, key=lambda r: int(r[0]))
+    assert [tuple(mem2[a:b]) for a, b in zip(ptr2[:-1], ptr2[1:])] == [tuple(r) for r in want2]
+    op = kp.OperatorKind.NORMALIZED_ADJACENCY
+    deg = rng.integers(1, 9, 30_000).astype(np.float64)
+    cdeg = deg[mem2[ptr2[:-1]]]
+    insts = M._instances(kp.MotifKind.CLOSED_TWIN, ptr2, mem2, (-1.0 / cdeg).tolist(),
+                         [{"degree": d, "weight": 1.0} for d in cdeg.tolist()], op)
+    for inst, r, d in zip(insts, want2, cdeg):
+        ref = M._build_instance(kp.MotifKind.CLOSED_TWIN, r, {"degree": float(d), "weight": 1.0}, op)
+        assert inst == ref and inst.multiplicity == ref.multiplicity and inst.auto
