@@ -1432,6 +1432,9 @@ __global__ void __launch_bounds__(256, KPM_LEAN_MINB) kpm_step_lean_kernel(const
 #ifndef KPM_G4_OWN
 #define KPM_G4_OWN 4
 #endif
+#ifndef KPM_G4_SEG
+#define KPM_G4_SEG 0  // row-segment consume loop for waves that span rows
+#endif
 template <int C>
 struct G4Tune {  // neighbours per wave, waves in flight, resident 256-thread CTAs
   static constexpr int wave = C == 1 ? KPM_G4_WAVE1 : (C == 2 ? KPM_G4_WAVE2 : 4);
@@ -1554,9 +1557,17 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
         asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(j[4 * q]), "=r"(j[4 * q + 1]), "=r"(j[4 * q + 2]), "=r"(j[4 * q + 3])
                      : "r"(ca + 16 * q));
+#if KPM_G4_SEG
+      if (cnt < WAVE) {
+#pragma unroll
+        for (int k = 1; k < WAVE; ++k)
+          if (k >= cnt) j[k] = j[0];  // a valid row; its bytes land unused
+      }
+#else
 #pragma unroll
       for (int k = 1; k < WAVE; ++k)
         if (k >= cnt) j[k] = j[0];  // a valid row; its bytes land unused
+#endif
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                    "r"((uint32_t)WAVE * rbytes)
                    : "memory");
@@ -1673,10 +1684,21 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       for (int k = 0; k < WAVE; ++k) add_one(k);
       advance(e0 + WAVE);
     } else {
+#if KPM_G4_SEG
+      // row segments of the wave: the neighbours of one row are added without
+      // per-neighbour row-end checks; advance() then closes the row (and any
+      // empty rows after it)
+      for (int k = 0; k < cnt;) {
+        const int seg = min(cnt, (int)(rend - e0));
+        for (; k < seg; ++k) add_one(k);
+        advance(e0 + k);
+      }
+#else
       for (int k = 0; k < cnt; ++k) {
         add_one(k);
         advance(e0 + k + 1);
       }
+#endif
     }
     __syncwarp();  // the whole warp is done with the slot and its weights
     if (w + D < nw) {
