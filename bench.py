@@ -63,12 +63,18 @@ def _tiled(P):
 
 
 def _step_launches(P):
-    return -(-P // 64) if _tiled(P) else 1
+    # the 64-column tiles of one step run as one launch when ld % 64 == 0
+    # (KPM_FUSE_TILES, kpm_step.cu launch_c), else one launch per tile
+    ld = -(-P // 4) * 4
+    if not _tiled(P):
+        return 1
+    return 1 if ld % 64 == 0 and os.environ.get("KPM_FUSE_TILES", "1") != "0" else -(-P // 64)
 
 
 def _kernel_label(P):
     if _tiled(P):
-        return "kpm_step_g4_kernel<C=2,DBL> x%d column tiles (TMA gather4)" % _step_launches(P)
+        return ("kpm_step_g4_kernel<C=2,DBL>, %d 64-column tiles in %d launch(es) (TMA gather4)"
+                % (-(-P // 64), _step_launches(P)))
     if P <= 64 and os.environ.get("KPM_G4", "1") != "0":
         return "kpm_step_g4_kernel<DBL> (TMA gather4)"
     if os.environ.get("KPM_BULK", "2") != "0":
@@ -221,7 +227,11 @@ def run_ours(args):
     family = kp.make_probes(n, P * world, "rademacher", seed=prm.get("seed", 0))
     probes = family.column_slice(rank * P, (rank + 1) * P)
     run = Run(dev, P, _lib.MODE_DOS_DOUBLING, m_run)
-    run.set_probes(probes)
+    ctx.synchronize()
+    t0 = time.time()
+    run.set_probes(probes)  # seeded Rademacher columns generated in HBM
+    ctx.synchronize()
+    t_probes = time.time() - t0
     stream = torch.cuda.ExternalStream(ctx.stream, device=local)
     torch.cuda.set_device(local)
 
@@ -296,10 +306,11 @@ def run_ours(args):
                        "probes_per_gpu": P, "moments": M, "mode": "doubling",
                        "units_per_step": units_step, "parallelism": f"probe-shard x{world}",
                        "l2": "inputs larger than L2 (two %.1f GB blocks)" % (8 * n * P / 1e9),
-                       "graph_build_s": round(t_build, 3)},
+                       "graph_build_s": round(t_build, 3), "probe_gen_s": round(t_probes, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "frac_nominal_8tbs": round(achieved / 8000.0, 4),
                          "bytes_per_launch_model": bstep,
                          "bytes_per_launch_compulsory": _compulsory_bytes(n, nnz, P),
                          "kernel": _kernel_label(P),
@@ -386,12 +397,21 @@ def cpu_baseline(cfg, sample_probes=8, sample_steps=1, graph=None):
     t0 = time.perf_counter()
     orc.dos_contrib(op, z, sample_steps, threads=threads)
     dt = time.perf_counter() - t0
+    # SURVEY §8d also asks for threads=1 (the numpy glue is single-threaded,
+    # so cores scale poorly): 2 probe columns, one step
+    z1 = z[:, :2].copy()
+    t0 = time.perf_counter()
+    orc.dos_contrib(op, z1, sample_steps, threads=1)
+    dt1 = time.perf_counter() - t0
     return {"value": round(nnz * sample_probes * sample_steps / dt / 1e9, 4),
             "unit": "G nnz*probe*moment/s", "cores": threads,
             "kind": "reference" if engine == "ref" else "port",
             "sample": (f"{sample_steps} recurrence step(s) (dos_moments m_max={sample_steps}) "
                        f"over {sample_probes} of {P} probes on the full {cfg.upper()} graph "
-                       f"(nnz={nnz}); {dt:.2f} s; reference Cython csr_matvec + numpy glue")}
+                       f"(nnz={nnz}); {dt:.2f} s; reference Cython csr_matvec + numpy glue"),
+            "single_thread": {"value": round(nnz * 2 * sample_steps / dt1 / 1e9, 4),
+                              "cores": 1,
+                              "sample": f"{sample_steps} step(s) over 2 probe columns; {dt1:.2f} s"}}
 
 
 def run_reference(args):

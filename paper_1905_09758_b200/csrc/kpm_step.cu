@@ -81,6 +81,8 @@ struct StepParams {
   int g4;                  // TMA gather4 light path: 0 off, 1 for C <= 2, 2 all layouts
   int lean;                // per-lane async gathers for C <= 2 (light_lean)
   int g4hint;              // gather4 L2 hint experiment: 0 none, 1 evict_last, 2 evict_first
+  int ntiles;              // gather4: light items per chunk = 64-column tiles of one launch
+  int fuse_tiles;          // run all 64-column tiles of a step as one launch
   int64_t hub_off;         // dynamic smem (doubles) of warp 0's hub ring (kpm_step_kernel)
   unsigned long long *trace;  // KPM_TRACE: per work item (start ns, end ns, smid<<32|warp)
 };
@@ -126,6 +128,7 @@ __device__ __forceinline__ const double *gather_row(const StepParams &p, uint32_
 // 52.7 ms step at P = 32, profiles/r01_trace_report.json).  Products h_ij*X[j,c] are
 // formed in parallel and added in neighbour order through shuffles.
 constexpr int kSlice = 4;
+constexpr int kTileW = 64;  // column tile of the 4-column layouts' gather4 passes
 constexpr int kHubDepth = 16;
 // per-warp hub ring: rows [kHubDepth][32] + dinv_j [kHubDepth][8] doubles,
 // col ids [2*kHubDepth][8] int32
@@ -1480,14 +1483,15 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm,
 
 template <int C, int MODE, bool EXPL, bool FIRST>
 __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap *tm, int chunk,
-                                         double *base, uint32_t &ophase, uint32_t &wphase) {
+                                         const int64_t col0, const int64_t tw, double *base,
+                                         uint32_t &ophase, uint32_t &wphase) {
   using L = G4<C, MODE, EXPL, FIRST>;
   constexpr int D = L::D, R = L::R, W = L::W, NOP = L::NOP, WAVE = L::WAVE;
   const int lane = threadIdx.x & 31;
   const int64_t ld = p.ld;
   // this launch's column tile [col0, col0 + tw): lane l owns columns col0 + [lC, lC + C)
-  const int64_t c0 = p.col0 + (int64_t)lane * C;
-  const bool active = (int64_t)lane * C < p.tw;
+  const int64_t c0 = col0 + (int64_t)lane * C;
+  const bool active = (int64_t)lane * C < tw;
   const int r0 = p.chunk_start[chunk], r1 = p.chunk_start[chunk + 1];
   double s1[C], s2[C];
 #pragma unroll
@@ -1506,7 +1510,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
   const uint32_t own_sa = col_sa + L::col_d * 8;
   uint64_t *wbar = reinterpret_cast<uint64_t *>(base + L::warp_d - L::bar_d);
   uint64_t *obar = wbar + D;
-  const uint32_t rbytes = (uint32_t)p.tw * 8u;  // one gathered row segment in shared memory
+  const uint32_t rbytes = (uint32_t)tw * 8u;  // one gathered row segment in shared memory
 
   int wb = r0;
   int64_t wrp = p.row_ptr[min(r0 + lane, r1)];
@@ -1580,12 +1584,12 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
           asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll
         for (int q = 0; q < WAVE / 4; ++q)
-          tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)p.col0, j[4 * q], j[4 * q + 1],
+          tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
                            j[4 * q + 2], j[4 * q + 3], bar, pol);
       } else {
 #pragma unroll
         for (int q = 0; q < WAVE / 4; ++q)
-          tma_gather4(dst + 4 * q * rbytes, tm, (int)p.col0, j[4 * q], j[4 * q + 1], j[4 * q + 2],
+          tma_gather4(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1], j[4 * q + 2],
                       j[4 * q + 3], bar);
       }
     }
@@ -1732,7 +1736,9 @@ kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
   uint32_t ophase = 0, wphase = 0;
-  const int64_t total = p.n_heavy_tasks + p.n_chunks;
+  // light items: ntiles column tiles x n_chunks (tile-major); ntiles > 1 only
+  // for the fused 64-column tiles of a 4-column layout (ld % 64 == 0)
+  const int64_t total = p.n_heavy_tasks + (int64_t)p.ntiles * p.n_chunks;
   for (;;) {
     unsigned long long item = 0;
     if (lane == 0) item = atomicAdd(p.queue, 1ull);
@@ -1742,8 +1748,14 @@ kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
     if ((int64_t)item < p.n_heavy_tasks) {
       heavy_task<MODE, EXPL, FIRST>(p, (int64_t)item, base);
     } else {
-      const int chunk = p.chunk_order[(int64_t)item - p.n_heavy_tasks];
-      light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, base, ophase, wphase);
+      const int64_t li = (int64_t)item - p.n_heavy_tasks;
+      const int64_t t = li / p.n_chunks;
+      const int chunk = p.chunk_order[li - t * p.n_chunks];
+      if (p.ntiles > 1)
+        light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0 + t * kTileW, kTileW, base, ophase,
+                                       wphase);
+      else
+        light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0, p.tw, base, ophase, wphase);
     }
     trace_item(p, item, t0);
   }
@@ -1976,7 +1988,7 @@ static cudaError_t launch_g4_k(const kpm_run *r, const StepParams &p, const CUte
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  const int64_t items = p.n_chunks + p.n_heavy_tasks;
+  const int64_t items = (int64_t)p.ntiles * p.n_chunks + p.n_heavy_tasks;
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) != cudaSuccess ||
       nb < 1) {
@@ -2022,6 +2034,14 @@ static cudaError_t launch_c(const kpm_run *r, const StepParams &p, bool expl, bo
     // every column's sums are unchanged, so the results are bitwise the same
     if (C == 4 && MODE != MODE_LDOS && p.tile && p.g4 && r->tm_tile_ok && p.nparts <= 1 &&
         blk >= 0) {
+      if (p.fuse_tiles && p.ld % kTileW == 0) {
+        // one launch over every tile: hub slices span the full width, light
+        // items are (tile, chunk) pairs, so the second tile's chunks fill the
+        // first tile's tail
+        StepParams q = p;
+        q.ntiles = (int)(p.ld / kTileW);
+        return launch_g4<2, MODE>(r, q, expl, first, r->tm[blk][1], st);
+      }
       for (int64_t t0 = 0; t0 < p.ld; t0 += 64) {
         StepParams q = p;
         q.col0 = t0;
@@ -2148,6 +2168,9 @@ static StepParams base_params(const kpm_run *r) {
   if (const char *e = getenv("KPM_LEAN")) p.lean = atoi(e);
   p.g4hint = 0;
   if (const char *e = getenv("KPM_G4_HINT")) p.g4hint = atoi(e);
+  p.ntiles = 1;
+  p.fuse_tiles = 1;  // 64-column tiles of one step in one launch (KPM_FUSE_TILES=0: per tile)
+  if (const char *e = getenv("KPM_FUSE_TILES")) p.fuse_tiles = atoi(e);
   p.bulk = 2;  // bulk-copy gathers in every layout (KPM_BULK=1: 4-column only, 0: none)
   if (const char *e = getenv("KPM_BULK")) p.bulk = atoi(e);
   // hot rows (L2 evict_last in the bulk path): the highest-degree rows whose
@@ -2529,8 +2552,10 @@ int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
     const char *trace_path = getenv("KPM_TRACE");
     const int trace_step = getenv("KPM_TRACE_STEP") ? atoi(getenv("KPM_TRACE_STEP")) : 2;
     const int64_t trace_items = r->g->n_chunks + p.n_heavy_tasks;
-    if (trace_path && r->done_steps == trace_step && trace_items > 0)
+    if (trace_path && r->done_steps == trace_step && trace_items > 0) {
       KPM_CUDA(cudaMallocAsync(&p.trace, sizeof(unsigned long long) * 3 * trace_items, st));
+      p.fuse_tiles = 0;  // the trace layout is one item per chunk
+    }
     KPM_CUDA(launch_step(r, p, false, first, st));
     if (p.trace) {
       std::vector<unsigned long long> tr(3 * trace_items);
