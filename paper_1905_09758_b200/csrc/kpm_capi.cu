@@ -85,6 +85,7 @@ int kpm_init(int device, kpm_ctx **out) {
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
   c->persist_max = prop.persistingL2CacheMaxSize;
+  c->l2_bytes = prop.l2CacheSize;
   // L2 set-aside for evict_last ("persisting") lines: KPM_PERSIST_MB (-1 = the
   // device maximum, 0 = none)
   if (const char *pm = getenv("KPM_PERSIST_MB")) {

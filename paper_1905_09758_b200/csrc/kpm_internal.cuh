@@ -60,6 +60,7 @@ struct kpm_ctx {
   int device = 0;
   int sm_count = 148;
   size_t persist_max = 0;  // cudaDeviceProp::persistingL2CacheMaxSize
+  size_t l2_bytes = 126u << 20;  // cudaDeviceProp::l2CacheSize
   cudaStream_t stream = nullptr;
 };
 

@@ -83,6 +83,8 @@ struct StepParams {
   int g4hint;              // gather4 L2 hint experiment: 0 none, 1 evict_last, 2 evict_first
   int ntiles;              // gather4: light items per chunk = 64-column tiles of one launch
   int fuse_tiles;          // run all 64-column tiles of a step as one launch
+  int g4hot;               // hot-ordered gather4 waves with L2 policies (light_g4 HOT)
+  double hot_dinv_g4;      // hot rows of the gather4 path: dinv_j <= hot_dinv_g4
   int64_t hub_off;         // dynamic smem (doubles) of warp 0's hub ring (kpm_step_kernel)
   unsigned long long *trace;  // KPM_TRACE: per work item (start ns, end ns, smid<<32|warp)
 };
@@ -1453,8 +1455,8 @@ struct G4 {
   static constexpr int W = 32 * C;
   static constexpr int slot_d = ((WAVE * W * 8 + 127) / 128) * 128 / 8;  // one wave's rows
   static constexpr int rows_d = D * slot_d;
-  static constexpr int wv_d = D * WAVE;
-  static constexpr int col_d = D * WAVE;  // [2D][WAVE] int32
+  static constexpr int wv_d = 2 * D * WAVE;   // [2D][WAVE] doubles (hot order: 2 slots at D=1)
+  static constexpr int col_d = 2 * D * WAVE;  // [4D][WAVE] int32 (default order uses 2D)
   static constexpr int own_d = R * (NOP > 0 ? NOP : 1) * W;
   static constexpr int bar_d = D + R;
   static constexpr int data_d = rows_d + wv_d + col_d + own_d;
@@ -1481,12 +1483,22 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm,
       : "memory");
 }
 
-template <int C, int MODE, bool EXPL, bool FIRST>
+// HOT (hot-ordered waves, D == 1, implicit values only): each wave's weights
+// dinv_j are fetched one wave ahead of its rows, so the issuing warp knows
+// which neighbours are hot (dinv_j <= hot_dinv_g4: the highest-degree rows
+// whose segments fill the hot budget of L2) before the gathers go out.  The
+// wave's rows land hot-first in shared memory (stable partition), so whole
+// gather4 groups carry one L2 policy: all-hot groups evict_last, all-cold
+// groups evict_first, a mixed group none.  The consumer still adds neighbour k
+// of the wave in CSR order, reading its row from position pos_k (one shuffle),
+// so sums and results are bitwise those of the default order.
+template <int C, int MODE, bool EXPL, bool FIRST, bool HOT>
 __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap *tm, int chunk,
                                          const int64_t col0, const int64_t tw, double *base,
                                          uint32_t &ophase, uint32_t &wphase) {
   using L = G4<C, MODE, EXPL, FIRST>;
   constexpr int D = L::D, R = L::R, W = L::W, NOP = L::NOP, WAVE = L::WAVE;
+  static_assert(!HOT || (D == 1 && !EXPL), "hot-ordered waves need D == 1 and dinv weights");
   const int lane = threadIdx.x & 31;
   const int64_t ld = p.ld;
   // this launch's column tile [col0, col0 + tw): lane l owns columns col0 + [lC, lC + C)
@@ -1541,7 +1553,20 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(obar + sl))
                  : "memory");
   };
-  auto col_slot = [&](int w) { return col_sa + (uint32_t)((w % (2 * D)) * WAVE * 4); };
+  auto col_slot = [&](int w) {
+    return col_sa + (uint32_t)((w % (HOT ? 4 : 2 * D)) * WAVE * 4);
+  };
+  auto wv_slot = [&](int w) { return wv_sa + (uint32_t)((w % (HOT ? 2 : D)) * WAVE * 8); };
+  int posw = 0;  // HOT: this lane's neighbour's row position in the wave being consumed
+  // HOT: weights of wave w (its col ids have landed)
+  auto issue_weight = [&](int w) {
+    const int e = w * WAVE + lane;
+    if (lane < WAVE && e < nnz) {
+      int jl;
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jl) : "r"(col_slot(w) + lane * 4));
+      cp_async_8(wv_slot(w) + lane * 8, p.dinv + jl);
+    }
+  };
   auto issue_col = [&](int w) {
     const int e = w * WAVE + lane;
     if (lane < WAVE && e < nnz) cp_async_4(col_slot(w) + lane * 4, p.col + K0 + e);
@@ -1553,6 +1578,25 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     const int cnt = min(WAVE, nnz - w * WAVE);
     const uint32_t ca = col_slot(w);
     const uint32_t bar = smem_u32(wbar + sl);
+    int nh = 0;
+    if constexpr (HOT) {
+      // stable hot-first partition of the wave's row ids, in place
+      int jk = 0;
+      bool hot = false;
+      if (lane < cnt) {
+        double wk;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jk) : "r"(ca + lane * 4));
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wk) : "r"(wv_slot(w) + lane * 8));
+        hot = wk <= p.hot_dinv_g4;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, hot);
+      nh = __popc(m);
+      const int below = __popc(m & ((1u << lane) - 1u));
+      posw = hot ? below : nh + lane - below;
+      __syncwarp();
+      if (lane < cnt) asm volatile("st.shared.b32 [%0], %1;" ::"r"(ca + posw * 4), "r"(jk) : "memory");
+      __syncwarp();
+    }
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads of the slot
       int j[WAVE];
@@ -1576,7 +1620,23 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
                    "r"((uint32_t)WAVE * rbytes)
                    : "memory");
       const uint32_t dst = rows_sa + sl * (uint32_t)(L::slot_d * 8);
-      if (p.g4hint) {
+      if constexpr (HOT) {
+        uint64_t pl, pf;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+#pragma unroll
+        for (int q = 0; q < WAVE / 4; ++q) {
+          if (4 * q + 4 <= nh)
+            tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
+                             j[4 * q + 2], j[4 * q + 3], bar, pl);
+          else if (4 * q >= nh)
+            tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
+                             j[4 * q + 2], j[4 * q + 3], bar, pf);
+          else
+            tma_gather4(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
+                        j[4 * q + 2], j[4 * q + 3], bar);
+        }
+      } else if (p.g4hint) {
         uint64_t pol;
         if (p.g4hint == 1)
           asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -1593,7 +1653,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
                       j[4 * q + 3], bar);
       }
     }
-    if (lane < cnt) {
+    if (!HOT && lane < cnt) {
       const uint32_t wd = wv_sa + (sl * WAVE + lane) * 8;
       if constexpr (EXPL) {
         cp_async_8(wd, p.vals + K0 + w * WAVE + lane);
@@ -1611,17 +1671,36 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
                    : "memory");
   };
 
+  if constexpr (HOT) {
+    // cols two waves and weights one wave ahead of the rows
+    issue_col(0);
+    issue_col(1);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    issue_weight(0);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
 #pragma unroll
-  for (int w = 0; w < 2 * D; ++w) issue_col(w);
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
+    for (int r = 0; r < R; ++r) issue_own(r0 + r);
+    if (nw > 0) {
+      issue_wave(0);
+      issue_weight(1);
+      issue_col(2);
+      arrive_wave(0);
+    }
+  } else {
 #pragma unroll
-  for (int r = 0; r < R; ++r) issue_own(r0 + r);
+    for (int w = 0; w < 2 * D; ++w) issue_col(w);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
 #pragma unroll
-  for (int w = 0; w < D; ++w) {
-    if (w < nw) {
-      issue_wave(w);
-      arrive_wave(w);
+    for (int r = 0; r < R; ++r) issue_own(r0 + r);
+#pragma unroll
+    for (int w = 0; w < D; ++w) {
+      if (w < nw) {
+        issue_wave(w);
+        arrive_wave(w);
+      }
     }
   }
 
@@ -1672,11 +1751,17 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     const int e0 = w * WAVE;
     const int cnt = min(WAVE, nnz - e0);
     const uint32_t slot = rows_sa + sl * (uint32_t)(L::slot_d * 8) + my_col;
+    const uint32_t wslot = HOT ? wv_slot(w) : wv_sa + sl * WAVE * 8;
     auto add_one = [&](int k) {
       double v[C];
-      lds_cols<C>(slot + k * rbytes, v);
+      if constexpr (HOT) {
+        const int pk = __shfl_sync(0xffffffffu, posw, k);
+        lds_cols<C>(slot + pk * rbytes, v);
+      } else {
+        lds_cols<C>(slot + k * rbytes, v);
+      }
       double wv;
-      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wv) : "r"(wv_sa + (sl * WAVE + k) * 8));
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wv) : "r"(wslot + k * 8));
       double h;
       if constexpr (EXPL) h = wv;
       else h = __dmul_rn(di, wv);  // (1*dinv_i)*dinv_j, operators.py:110
@@ -1706,8 +1791,14 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     }
     __syncwarp();  // the whole warp is done with the slot and its weights
     if (w + D < nw) {
-      issue_wave(w + D);
-      issue_col(w + 2 * D);
+      if constexpr (HOT) {
+        issue_wave(w + 1);
+        issue_weight(w + 2);
+        issue_col(w + 3);
+      } else {
+        issue_wave(w + D);
+        issue_col(w + 2 * D);
+      }
       arrive_wave(w + D);
     }
   }
@@ -1721,7 +1812,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
   }
 }
 
-template <int C, int MODE, bool EXPL, bool FIRST>
+template <int C, int MODE, bool EXPL, bool FIRST, bool HOT>
 __global__ void __launch_bounds__(256, G4Tune<C>::minb)
 kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
   using L = G4<C, MODE, EXPL, FIRST>;
@@ -1752,10 +1843,10 @@ kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
       const int64_t t = li / p.n_chunks;
       const int chunk = p.chunk_order[li - t * p.n_chunks];
       if (p.ntiles > 1)
-        light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0 + t * kTileW, kTileW, base, ophase,
-                                       wphase);
+        light_g4<C, MODE, EXPL, FIRST, HOT>(p, &tm, chunk, p.col0 + t * kTileW, kTileW, base,
+                                            ophase, wphase);
       else
-        light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0, p.tw, base, ophase, wphase);
+        light_g4<C, MODE, EXPL, FIRST, HOT>(p, &tm, chunk, p.col0, p.tw, base, ophase, wphase);
     }
     trace_item(p, item, t0);
   }
@@ -1979,10 +2070,10 @@ static cudaError_t launch_lean_k(const kpm_run *r, const StepParams &p, cudaStre
   return cudaGetLastError();
 }
 
-template <int C, int MODE, bool EXPL, bool FIRST>
+template <int C, int MODE, bool EXPL, bool FIRST, bool HOT = false>
 static cudaError_t launch_g4_k(const kpm_run *r, const StepParams &p, const CUtensorMap &tm,
                                cudaStream_t st) {
-  void (*kern)(StepParams, CUtensorMap) = kpm_step_g4_kernel<C, MODE, EXPL, FIRST>;
+  void (*kern)(StepParams, CUtensorMap) = kpm_step_g4_kernel<C, MODE, EXPL, FIRST, HOT>;
   const int threads = 256;
   const size_t smem = (size_t)(threads / 32) * G4<C, MODE, EXPL, FIRST>::warp_d * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2010,6 +2101,12 @@ static cudaError_t launch_g4(const kpm_run *r, const StepParams &p, bool expl, b
                              const CUtensorMap &tm, cudaStream_t st) {
   if (expl && first) return launch_g4_k<C, MODE, true, true>(r, p, tm, st);
   if (expl) return launch_g4_k<C, MODE, true, false>(r, p, tm, st);
+  if constexpr (C <= 2 && G4Tune<C>::d == 1) {
+    if (p.g4hot && p.hot_dinv_g4 > 0.0) {
+      if (first) return launch_g4_k<C, MODE, false, true, true>(r, p, tm, st);
+      return launch_g4_k<C, MODE, false, false, true>(r, p, tm, st);
+    }
+  }
   if (first) return launch_g4_k<C, MODE, false, true>(r, p, tm, st);
   return launch_g4_k<C, MODE, false, false>(r, p, tm, st);
 }
@@ -2189,6 +2286,30 @@ static StepParams base_params(const kpm_run *r) {
     }
     if (const char *e = getenv("KPM_HOT_DEGREE")) hot_deg = atof(e);
     if (hot_deg > 0) p.hot_dinv = 1.0 / sqrt(hot_deg);
+  }
+  // hot rows of the gather4 path (hot-ordered waves): same rule over the
+  // gathered segment (64-column tiles for the 4-column layouts)
+  p.hot_dinv_g4 = -1.0;
+  {
+    double hot_bytes = 64.0 * 1024 * 1024;
+    if (const char *e = getenv("KPM_HOT_MB_G4")) hot_bytes = atof(e) * 1024 * 1024;
+    const bool tiled = r->cpl == 4 && r->ld > kTileW;
+    const int64_t seg = tiled ? kTileW : r->ld;
+    // default (measured, profiles/r01_g4_hot_ab.log): on for the 64-column
+    // tiles when one tile's gathered block is > 200x the L2 (C5: 34 GB, DRAM
+    // -9.5%, step -2.7%); off below that, where plain LRU already keeps the
+    // popular rows and the ordering only costs instructions (C3: +2.6%), and
+    // for the 1-column layout (C3/C5 P=32: +4%)
+    p.g4hot = tiled && 8.0 * (double)seg * (double)g->n > 200.0 * (double)g->ctx->l2_bytes;
+    if (const char *e = getenv("KPM_G4_HOT")) p.g4hot = atoi(e);
+    const double budget = hot_bytes / (8.0 * (double)seg);
+    double rows = 0.0, hot_deg = 0.0;
+    for (int b = 63; b >= 0; --b) {
+      rows += (double)g->deg_log2_hist[b];
+      if (rows > budget) break;
+      hot_deg = std::ldexp(1.0, b);
+    }
+    if (hot_deg > 0) p.hot_dinv_g4 = 1.0 / sqrt(hot_deg);
   }
   return p;
 }

@@ -509,6 +509,9 @@ def test_filtered_probes_stay_on_device(golden, kpm_ctx):
 # oracle's restated recurrence (the reference's _row order, no FMA).
 _PATHS = {
     "tiles": {},  # default: gather4, 4-column layouts as 64-column passes
+    # hot-ordered gather4 waves, a hot set small enough that waves mix hot and cold rows
+    "hot": {"KPM_G4_HOT": "1", "KPM_HOT_MB_G4": "0.02"},
+    "tiles-unfused": {"KPM_FUSE_TILES": "0"},
     "g4": {"KPM_G4": "2", "KPM_TILE": "0"},
     "lean": {"KPM_G4": "0"},
     "bulk": {"KPM_G4": "0", "KPM_LEAN": "0"},
@@ -520,7 +523,8 @@ _PATHS = {
 @pytest.mark.parametrize("P", [4, 20, 30, 32, 36, 64, 100, 128])
 @pytest.mark.parametrize("hubs", [False, True])
 def test_light_paths_bitexact(oracle, kpm_ctx, monkeypatch, path, P, hubs):
-    for k in ("KPM_G4", "KPM_TILE", "KPM_LEAN", "KPM_BULK", "KPM_HEAVY_DEGREE"):
+    for k in ("KPM_G4", "KPM_TILE", "KPM_LEAN", "KPM_BULK", "KPM_HEAVY_DEGREE", "KPM_G4_HOT",
+              "KPM_HOT_MB_G4", "KPM_FUSE_TILES"):
         monkeypatch.delenv(k, raising=False)
     for k, v in _PATHS[path].items():
         monkeypatch.setenv(k, v)
