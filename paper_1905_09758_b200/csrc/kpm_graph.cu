@@ -388,8 +388,12 @@ int finish_graph(kpm_graph *g) {
     cudaFree(dmx);
     std::vector<int32_t> order(nch);
     for (int64_t c = 0; c < nch; ++c) order[c] = (int32_t)c;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int32_t x, int32_t y) { return mx[x] > mx[y]; });
+    // KPM_CHUNK_ORDER=1 (experiment): row-id order, so warps in flight work
+    // one contiguous id window of the graph
+    const char *eo = getenv("KPM_CHUNK_ORDER");
+    if (!(eo && atoi(eo) == 1))
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int32_t x, int32_t y) { return mx[x] > mx[y]; });
     KPM_CUDA(cudaMalloc(&g->chunk_order, sizeof(int32_t) * (nch > 0 ? nch : 1)));
     KPM_CUDA(cudaMemcpy(g->chunk_order, order.data(), sizeof(int32_t) * nch,
                         cudaMemcpyHostToDevice));
