@@ -1437,6 +1437,9 @@ __global__ void __launch_bounds__(256, KPM_LEAN_MINB) kpm_step_lean_kernel(const
 #ifndef KPM_G4_OWN
 #define KPM_G4_OWN 4
 #endif
+#ifndef KPM_G4_FMA
+#define KPM_G4_FMA 0
+#endif
 #ifndef KPM_G4_SEG
 #define KPM_G4_SEG 0  // row-segment consume loop for waves that span rows
 #endif
@@ -1766,7 +1769,12 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       if constexpr (EXPL) h = wv;
       else h = __dmul_rn(di, wv);  // (1*dinv_i)*dinv_j, operators.py:110
 #pragma unroll
-      for (int c = 0; c < C; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[c]));
+      for (int c = 0; c < C; ++c)
+#if KPM_G4_FMA  // experiment: fused multiply-add (not the reference's rounding)
+        acc[c] = __fma_rn(h, v[c], acc[c]);
+#else
+        acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[c]));
+#endif
     };
     if (cnt == WAVE && e0 + WAVE <= rend) {
 #pragma unroll
