@@ -73,6 +73,12 @@ int kpm_host_alloc(int64_t bytes, void **out);
 /* free / total device memory of the context's GPU (probe batch sizing) */
 int kpm_mem_info(kpm_ctx *ctx, int64_t *free_bytes, int64_t *total_bytes);
 int kpm_host_free(void *ptr);
+/* Touch every page of a caller-owned (pageable) host result buffer with
+ * `threads` host threads (<= 0: up to 16), after advising transparent huge
+ * pages, so a following D2H copy does not pay the first-touch page faults on
+ * one thread.  The buffer's contents are overwritten.  Host-only; meant to
+ * run while queued kernels execute (C2: 808 MB of per-node moments). */
+int kpm_host_prefault(void *ptr, int64_t bytes, int threads);
 
 /* ------------------------------------------------------------- graphs --- */
 /* Device graph loader (K1-K3).  Replaces graph.py:69-81 _csr_from_canonical

@@ -56,6 +56,7 @@ SIGNATURES = {
     "kpm_memcpy": (_c_int, [_c_vp, _c_vp, _c_vp, _c_i64, _c_int]),
     "kpm_host_alloc": (_c_int, [_c_i64, _PP]),
     "kpm_host_free": (_c_int, [_c_vp]),
+    "kpm_host_prefault": (_c_int, [_c_vp, _c_i64, _c_int]),
     "kpm_mem_info": (_c_int, [_c_vp, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)]),
     "kpm_graph_from_edges": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_i64, _c_int, _PP]),
     "kpm_graph_from_csr": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_i64, _c_vp, _c_dbl,
@@ -157,6 +158,16 @@ def check(rc: int, what: str = "") -> None:
     if rc == KPM_ENOMEM:
         raise MemoryError(msg)
     raise KpmLibraryError(f"libkpm status {rc}: {msg}")
+
+
+def prefault(a, threads=0):
+    """Page in a fresh host result array on host threads (kpm_host_prefault)
+    so the D2H copy into it does not fault page by page; its contents are
+    overwritten."""
+    if a.nbytes:
+        check(load().kpm_host_prefault(a.ctypes.data, a.nbytes, int(threads)),
+              "host_prefault")
+    return a
 
 
 def ptr(a) -> int | None:

@@ -1,6 +1,9 @@
 // libkpm C-ABI: context, memory and error plumbing (include/kpm.h).
 #include <cstdlib>
 #include <cstring>
+#include <sys/mman.h>
+#include <thread>
+#include <vector>
 
 #include "kpm_internal.cuh"
 
@@ -196,3 +199,36 @@ int kpm_host_free(void *ptr) {
 }
 
 }  // extern "C"
+
+int kpm_host_prefault(void *ptr, int64_t bytes, int threads) {
+  KPM_CHECK_ARG(bytes >= 0, "negative size");
+  if (!ptr || bytes == 0) return KPM_OK;
+  const uintptr_t pg = 4096, a = (uintptr_t)ptr, e = a + (uintptr_t)bytes;
+  const uintptr_t lo = (a + pg - 1) & ~(pg - 1), hi = e & ~(pg - 1);
+  if (hi > lo) madvise((void *)lo, hi - lo, MADV_HUGEPAGE);  // advisory only
+  if (threads <= 0) {
+    const unsigned hc = std::thread::hardware_concurrency();
+    threads = (int)(hc == 0 ? 1 : (hc < 16 ? hc : 16));
+  }
+  const uintptr_t base = a & ~(pg - 1);
+  const int64_t pages = (int64_t)((e - base + pg - 1) / pg);  // pages the buffer spans
+  if (pages < 4 * threads) threads = 1;
+  auto touch = [=](int64_t p0, int64_t p1) {
+    volatile char *c = (volatile char *)ptr;
+    for (int64_t q = p0; q < p1; ++q) {
+      const uintptr_t at = base + (uintptr_t)q * pg;
+      c[(at > a ? at : a) - a] = 0;  // first byte of page q inside the buffer
+    }
+  };
+  if (threads == 1) {
+    touch(0, pages);
+    return KPM_OK;
+  }
+  std::vector<std::thread> ts;
+  for (int t = 0; t < threads; ++t) {
+    const int64_t p0 = pages * t / threads, p1 = pages * (t + 1) / threads;
+    ts.emplace_back(touch, p0, p1);
+  }
+  for (auto &t : ts) t.join();
+  return KPM_OK;
+}

@@ -246,8 +246,9 @@ def pdos_moments(sop, probes: ProbeMatrix, m_max: int, normalized=True, threads=
         run = Run(dev, nz, _lib.MODE_LDOS, m_max, 0 if normalized else _lib.LDOS_RAW)
         try:
             run.set_probes(probes)
-            run.advance()
+            run.advance()  # queued; the host pages the result in meanwhile
             values = np.empty((n, m_max + 1))
+            _lib.prefault(values)
             run.result(values, probes.trace_scale)
         finally:
             run.free()

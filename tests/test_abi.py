@@ -60,3 +60,21 @@ def test_sm100a_code_only():
     out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
     assert "sm_90" not in out.stdout
+
+
+def test_host_prefault_is_host_only_and_bounds_safe():
+    """kpm_host_prefault pages in caller buffers (aligned or not, tiny or
+    multi-page, any thread count) without a GPU and rejects negative sizes."""
+    import numpy as np
+
+    from paper_1905_09758_b200 import _lib
+
+    for nbytes, off in ((1, 0), (4095, 1), (4097, 3), (1 << 22, 5), ((1 << 22) + 7, 0)):
+        buf = np.full(nbytes + off, 7, dtype=np.uint8)[off:]
+        for th in (0, 1, 3, 16):
+            _lib.prefault(buf, th)
+        assert buf[0] == 0 and np.all(buf[buf != 0] == 7)
+    empty = np.empty(0)
+    _lib.prefault(empty)
+    assert _lib.load().kpm_host_prefault(None, 0, 0) == 0
+    assert _lib.load().kpm_host_prefault(empty.ctypes.data, -1, 0) != 0
