@@ -200,3 +200,34 @@ def test_c5_rmat26_one_gpu_batch(kpm_ctx):
     dd = kp.dos_moments(sop, probes, 20, doubling=False)
     assert d.values[0] == pytest.approx(1.0, abs=1e-14)
     assert _normwise(d.values, dd.values) <= 1e-9
+
+
+def test_c5_rmat26_csr_rowranges_bitexact(oracle, kpm_ctx):
+    """SURVEY §8c, CSR bit-exactness at C5 by row ranges: the oracle restates
+    _csr_from_canonical on every draw touching rows [a, b) (the generator run
+    in 2^27-draw chunks), and rows [a, b) of the device CSR (row_ptr offsets,
+    int32 col_idx, d^-1/2) must equal it bit for bit.  Ranges: the highest-
+    degree ids [0, 4096), a middle window and the sparse tail."""
+    scale, ef, seed = 26, 16, 4
+    n = 1 << scale
+    dev = kp.DeviceGraph.rmat(scale, ef, seed)
+    rp, ci, dinv = dev.export()
+    ranges = [(0, 4096), ((1 << 25), (1 << 25) + (1 << 18)), (n - (1 << 18), n)]
+    n_draws = ef << scale
+    chunk = 1 << 27
+    sel = [([], []) for _ in ranges]
+    for e0 in range(0, n_draws, chunk):
+        u, v = oracle.rmat_edges(scale, n_draws, seed, e0=e0, count=min(chunk, n_draws - e0))
+        for (a, b), (su, sv) in zip(ranges, sel):
+            m = ((u >= a) & (u < b)) | ((v >= a) & (v < b))
+            su.append(u[m])
+            sv.append(v[m])
+        del u, v
+    for (a, b), (su, sv) in zip(ranges, sel):
+        orp, oci = oracle.csr_from_edges(n, np.concatenate(su), np.concatenate(sv))
+        want_rp = orp[a:b + 1] - orp[a]
+        got_rp = rp[a:b + 1] - rp[a]
+        assert np.array_equal(got_rp, want_rp), (a, b)
+        assert np.array_equal(ci[rp[a]:rp[b]], oci[orp[a]:orp[b]].astype(np.int32)), (a, b)
+        assert np.array_equal(dinv[a:b], oracle.dinv_of(orp[a:b + 1] - orp[a])), (a, b)
+        print("c5 rows", a, b, "nnz", int(rp[b] - rp[a]))
