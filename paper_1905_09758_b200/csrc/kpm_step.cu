@@ -1437,6 +1437,9 @@ __global__ void __launch_bounds__(256, KPM_LEAN_MINB) kpm_step_lean_kernel(const
 #ifndef KPM_G4_OWN
 #define KPM_G4_OWN 4
 #endif
+#ifndef KPM_G4_THREADS
+#define KPM_G4_THREADS 256
+#endif
 #ifndef KPM_G4_FMA
 #define KPM_G4_FMA 0
 #endif
@@ -2082,7 +2085,7 @@ template <int C, int MODE, bool EXPL, bool FIRST, bool HOT = false>
 static cudaError_t launch_g4_k(const kpm_run *r, const StepParams &p, const CUtensorMap &tm,
                                cudaStream_t st) {
   void (*kern)(StepParams, CUtensorMap) = kpm_step_g4_kernel<C, MODE, EXPL, FIRST, HOT>;
-  const int threads = 256;
+  const int threads = KPM_G4_THREADS;  // warps are independent; CTA size sets smem granularity
   const size_t smem = (size_t)(threads / 32) * G4<C, MODE, EXPL, FIRST>::warp_d * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
