@@ -225,10 +225,16 @@ int kpm_host_prefault(void *ptr, int64_t bytes, int threads) {
     return KPM_OK;
   }
   std::vector<std::thread> ts;
-  for (int t = 0; t < threads; ++t) {
-    const int64_t p0 = pages * t / threads, p1 = pages * (t + 1) / threads;
-    ts.emplace_back(touch, p0, p1);
+  int64_t done = 0;  // pages [0, done) are covered by started threads
+  try {
+    for (int t = 0; t < threads; ++t) {
+      const int64_t p0 = pages * t / threads, p1 = pages * (t + 1) / threads;
+      ts.emplace_back(touch, p0, p1);
+      done = p1;
+    }
+  } catch (...) {  // no thread available: the caller's thread finishes the rest
   }
+  touch(done, pages);
   for (auto &t : ts) t.join();
   return KPM_OK;
 }
