@@ -105,6 +105,18 @@ int kpm_graph_from_csr(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
                        const double *values, double shift, double scale,
                        kpm_graph **out);
 
+/* Copy a graph to another context (another GPU over NVLink/NVSwitch peer
+ * copies, or a second context on the same GPU): probe columns / LDOS shards
+ * of one dos_moments / pdos_moments call then run on every GPU of the process
+ * (the reference's `threads` knob, kpm.py:92-93, mapped to devices). */
+int kpm_graph_replicate(kpm_graph *src, kpm_ctx *ctx, kpm_graph **out);
+
+/* Same with int32 column indices (the device layout: no widening copy; a
+ * host CSR of 2e9 nonzeros is 8 GB instead of 16 GB). */
+int kpm_graph_from_csr32(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
+                         const int32_t *indices, int64_t nnz, const double *values,
+                         double shift, double scale, kpm_graph **out);
+
 int kpm_graph_info(kpm_graph *g, int64_t *n, int64_t *nnz, int64_t *max_degree);
 /* Copy the device CSR back (any pointer may be NULL): bit-exactness checks. */
 int kpm_graph_export(kpm_graph *g, int64_t *row_ptr, int32_t *col_idx,
@@ -172,6 +184,18 @@ int kpm_run_kernel_time(kpm_run *r, double *ms, int32_t *launches);
  * *bad_node, may be NULL) for a zero probe mass in normalized LDOS. */
 int kpm_run_result(kpm_run *r, double *out, double trace_scale,
                    int64_t *bad_node);
+/* LDOS runs: out may be NULL -- the values are finished in place and stay in
+ * the run's own n x (m_max+1) device buffer, returned by kpm_run_ldos_values
+ * (valid until kpm_run_free), e.g. for kpm_ldos_histogram without a copy. */
+int kpm_run_ldos_values(kpm_run *r, const double **values);
+/* LDOS probe batches / GPU shards: dst's raw per-node sums and probe masses
+ * += src's (src may live on another GPU: peer copy).  Both runs must have run
+ * all their steps and not yet been finished by kpm_run_result; the zero-mass
+ * check and the normalisation then apply to the combined sums. */
+int kpm_run_accumulate(kpm_run *dst, kpm_run *src);
+/* Free the recurrence blocks of a completed run, keeping its results (the
+ * (m_max+1) x k contributions or the n x (m_max+1) LDOS sums). */
+int kpm_run_trim(kpm_run *r);
 /* Device pointer of the current T_k block and its row stride (tests). */
 int kpm_run_block(kpm_run *r, const double **t_k, int64_t *ld, int32_t *k_index);
 void kpm_run_free(kpm_run *r);

@@ -25,44 +25,91 @@ static int cmp_i64(const void *a, const void *b) {
 int64_t orc_csr_from_edges(int64_t n, const int64_t *u, const int64_t *v,
                            int64_t m, int flags, int64_t *row_ptr,
                            int64_t *col_idx) {
+  /* Counting scatter, then per-row sort + unique: the result (sorted unique
+   * neighbours per row) does not depend on the scatter order, so the passes
+   * run on OpenMP threads (atomic counters) and stay deterministic. */
   const int keep_loops = flags & 1;
   int64_t *cnt = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
   if (!cnt) return -1;
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(|| : bad)
   for (int64_t e = 0; e < m; ++e) {
     int64_t a = u[e], b = v[e];
-    if (a < 0 || b < 0 || a >= n || b >= n) { free(cnt); return -1; }
+    if (a < 0 || b < 0 || a >= n || b >= n) { bad = 1; continue; }
     if (a == b) {
-      if (keep_loops) cnt[a + 1]++;
+      if (keep_loops) {
+#pragma omp atomic
+        cnt[a + 1]++;
+      }
       continue;
     }
+#pragma omp atomic
     cnt[a + 1]++;
+#pragma omp atomic
     cnt[b + 1]++;
   }
+  if (bad) { free(cnt); return -1; }
   for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
   int64_t *pos = (int64_t *)malloc(((size_t)n + 1) * sizeof(int64_t));
   memcpy(pos, cnt, ((size_t)n + 1) * sizeof(int64_t));
+#pragma omp parallel for schedule(static)
   for (int64_t e = 0; e < m; ++e) {
-    int64_t a = u[e], b = v[e];
+    int64_t a = u[e], b = v[e], p;
     if (a == b) {
-      if (keep_loops) col_idx[pos[a]++] = a;
+      if (keep_loops) {
+#pragma omp atomic capture
+        p = pos[a]++;
+        col_idx[p] = a;
+      }
       continue;
     }
-    col_idx[pos[a]++] = b;
-    col_idx[pos[b]++] = a;
+#pragma omp atomic capture
+    p = pos[a]++;
+    col_idx[p] = b;
+#pragma omp atomic capture
+    p = pos[b]++;
+    col_idx[p] = a;
   }
   free(pos);
-  /* sort + unique per row, compact in place (row order preserved) */
+  /* sort + unique per row; each thread compacts a contiguous block of rows
+   * in place (row_ptr[i+1] holds the row's unique count for now), then the
+   * blocks are moved left in order */
+  int nt = 1;
+#pragma omp parallel
+  {
+#pragma omp single
+    nt = omp_get_num_threads();
+  }
+  int64_t *blk_lo = (int64_t *)malloc(sizeof(int64_t) * (nt + 1));
+  int64_t *blk_w = (int64_t *)malloc(sizeof(int64_t) * (nt + 1));
+  for (int t = 0; t <= nt; ++t) blk_lo[t] = n * t / nt;
+#pragma omp parallel num_threads(nt)
+  {
+    const int t = omp_get_thread_num();
+    int64_t w = cnt[blk_lo[t]];
+    for (int64_t i = blk_lo[t]; i < blk_lo[t + 1]; ++i) {
+      int64_t s = cnt[i], e = cnt[i + 1];
+      qsort(col_idx + s, (size_t)(e - s), sizeof(int64_t), cmp_i64);
+      const int64_t w0 = w;
+      for (int64_t jj = s; jj < e; ++jj) {
+        if (jj > s && col_idx[jj] == col_idx[jj - 1]) continue;
+        col_idx[w++] = col_idx[jj];
+      }
+      row_ptr[i + 1] = w - w0;
+    }
+    blk_w[t] = w - cnt[blk_lo[t]];
+  }
   int64_t w = 0;
   row_ptr[0] = 0;
-  for (int64_t i = 0; i < n; ++i) {
-    int64_t s = cnt[i], t = cnt[i + 1];
-    qsort(col_idx + s, (size_t)(t - s), sizeof(int64_t), cmp_i64);
-    for (int64_t jj = s; jj < t; ++jj) {
-      if (jj > s && col_idx[jj] == col_idx[jj - 1]) continue;
-      col_idx[w++] = col_idx[jj];
-    }
-    row_ptr[i + 1] = w;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t src = cnt[blk_lo[t]];
+    if (blk_w[t] && src != w)
+      memmove(col_idx + w, col_idx + src, sizeof(int64_t) * (size_t)blk_w[t]);
+    for (int64_t i = blk_lo[t]; i < blk_lo[t + 1]; ++i) row_ptr[i + 1] += row_ptr[i];
+    w += blk_w[t];
   }
+  free(blk_lo);
+  free(blk_w);
   free(cnt);
   return w;
 }
@@ -70,6 +117,7 @@ int64_t orc_csr_from_edges(int64_t n, const int64_t *u, const int64_t *v,
 /* graph.py:47-54 (deg = sum of unit weights, a loop counted once) and
  * operators.py:108-109: dinv = 1/sqrt(max(deg,1e-300)) if deg > 0 else 0. */
 void orc_dinv(int64_t n, const int64_t *row_ptr, double *dinv) {
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) {
     double deg = (double)(row_ptr[i + 1] - row_ptr[i]);
     dinv[i] = deg > 0 ? 1.0 / sqrt(deg) : 0.0;
@@ -80,6 +128,7 @@ void orc_dinv(int64_t n, const int64_t *row_ptr, double *dinv) {
 void orc_normadj_values(int64_t n, const int64_t *row_ptr,
                         const int64_t *col_idx, const double *dinv,
                         double *data) {
+#pragma omp parallel for schedule(dynamic, 4096)
   for (int64_t i = 0; i < n; ++i)
     for (int64_t jj = row_ptr[i]; jj < row_ptr[i + 1]; ++jj)
       data[jj] = (1.0 * dinv[i]) * dinv[col_idx[jj]];

@@ -166,6 +166,19 @@ def normadj_values(row_ptr, col_idx, dinv=None):
     return (1.0 * dinv[rows]) * dinv[col_idx]
 
 
+def normadj_values_c(row_ptr, col_idx, dinv):
+    """Same values as normadj_values (operators.py:110, (1.0*dinv[r])*dinv[c])
+    from the C restatement on all host threads, without numpy's row-index
+    temporaries (C5: 2.1e9 nonzeros)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+    di = np.ascontiguousarray(dinv, dtype=np.float64)
+    out = np.empty(ci.shape[0])
+    lib().orc_normadj_values(rp.shape[0] - 1, _ptr(rp, _I64P), _ptr(ci, _I64P), _ptr(di, _F64P),
+                             _ptr(out, _F64P))
+    return out
+
+
 # --------------------------------------------------------------------- SpMM
 def csr_matvec(indptr, indices, data, x, threads=1, engine="c"):
     """_kernels/__init__.py:33-46 csr_matvec with a chosen engine."""

@@ -61,6 +61,8 @@ SIGNATURES = {
     "kpm_graph_from_edges": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_i64, _c_int, _PP]),
     "kpm_graph_from_csr": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_i64, _c_vp, _c_dbl,
                                     _c_dbl, _PP]),
+    "kpm_graph_from_csr32": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_i64, _c_vp, _c_dbl,
+                                      _c_dbl, _PP]),
     "kpm_graph_info": (_c_int, [_c_vp, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64),
                                 ctypes.POINTER(_c_i64)]),
     "kpm_graph_export": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp]),
@@ -78,6 +80,10 @@ SIGNATURES = {
     "kpm_run_set_timing": (_c_int, [_c_vp, _c_int]),
     "kpm_run_kernel_time": (_c_int, [_c_vp, ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_i32)]),
     "kpm_run_result": (_c_int, [_c_vp, _c_vp, _c_dbl, ctypes.POINTER(_c_i64)]),
+    "kpm_run_ldos_values": (_c_int, [_c_vp, _PP]),
+    "kpm_run_accumulate": (_c_int, [_c_vp, _c_vp]),
+    "kpm_run_trim": (_c_int, [_c_vp]),
+    "kpm_graph_replicate": (_c_int, [_c_vp, _c_vp, _PP]),
     "kpm_run_block": (_c_int, [_c_vp, _PP, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i32)]),
     "kpm_run_free": (None, [_c_vp]),
     "kpm_dos_contrib": (_c_int, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_vp]),
@@ -110,7 +116,7 @@ SIGNATURES = {
 }
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()
 
 
 class KpmLibraryError(NetdosError, RuntimeError):
@@ -184,9 +190,11 @@ def ptr(a) -> int | None:
 
 
 class Context:
-    """One libkpm context (one GPU, one CUDA stream) per process and device."""
+    """A libkpm context: one GPU and its own CUDA stream.  ``get(device)`` is
+    the process's shared context of a device; ``pool`` adds further contexts
+    (their own streams) when a device is listed more than once."""
 
-    _by_device: dict[int, "Context"] = {}
+    _by_key: dict[tuple[int, int], "Context"] = {}
 
     def __init__(self, device: int = 0):
         lib = load()
@@ -196,14 +204,27 @@ class Context:
         self.handle = h.value
 
     @classmethod
-    def get(cls, device: int | None = None) -> "Context":
+    def get(cls, device: int | None = None, slot: int = 0) -> "Context":
         if device is None:
             device = default_device()
-        ctx = cls._by_device.get(device)
-        if ctx is None:
-            ctx = cls(device)
-            cls._by_device[device] = ctx
+        key = (int(device), int(slot))
+        with _lock:
+            ctx = cls._by_key.get(key)
+            if ctx is None:
+                ctx = cls(device)
+                cls._by_key[key] = ctx
         return ctx
+
+    @classmethod
+    def pool(cls, devices) -> list["Context"]:
+        """Contexts for a device list; a repeated device gets another slot."""
+        seen: dict[int, int] = {}
+        out = []
+        for d in devices:
+            k = seen.get(int(d), 0)
+            seen[int(d)] = k + 1
+            out.append(cls.get(int(d), k))
+        return out
 
     @property
     def stream(self) -> int:
@@ -225,6 +246,26 @@ def default_device() -> int:
         if v not in (None, ""):
             return int(v)
     return 0
+
+
+def devices_for(threads=1) -> list[int]:
+    """GPUs one moment call uses (the reference's ``threads``
+    knob, kpm.py:92-93 / NETDOS_THREADS cli.py:31-35, maps to a GPU count).
+    KPM_DEVICES ("0,1,...", "all"; a repeated id adds a context on that GPU)
+    wins; under torchrun (LOCAL_RANK set) a process keeps its own GPU; else
+    ``threads`` > 1 uses min(threads, visible GPUs) starting at the default
+    device."""
+    env = os.environ.get("KPM_DEVICES", "").strip()
+    if env:
+        if env == "all":
+            return list(range(device_count()))
+        return [int(x) for x in env.split(",") if x.strip()]
+    first = default_device()
+    if os.environ.get("LOCAL_RANK") not in (None, "") or int(threads or 1) <= 1:
+        return [first]
+    count = device_count()
+    want = min(int(threads), count)
+    return [(first + i) % count for i in range(want)]
 
 
 def device_count() -> int:

@@ -492,6 +492,14 @@ __global__ void idx64_to_32(const int64_t *__restrict__ in, int64_t m,
   }
 }
 
+__global__ void idx32_check(const int32_t *__restrict__ in, int64_t m, int64_t n, int *bad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = in[e];
+    if (x < 0 || x >= n) atomicOr(bad, 1);
+  }
+}
+
 }  // namespace kpm
 
 using namespace kpm;
@@ -586,15 +594,21 @@ int kpm_rmat_edges(kpm_ctx *ctx, int scale, uint64_t seed, uint32_t ta,
 }
 
 static int graph_from_csr_impl(kpm_ctx *ctx, int64_t n, int64_t n_cols, int64_t row0,
-                               const int64_t *indptr, const int64_t *indices, int64_t nnz,
-                               const double *values, double shift, double scale,
+                               const int64_t *indptr, const void *indices, int idx_bytes,
+                               int64_t nnz, const double *values, double shift, double scale,
                                kpm_graph **out);
 
 int kpm_graph_from_csr(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
                        const int64_t *indices, int64_t nnz,
                        const double *values, double shift, double scale,
                        kpm_graph **out) {
-  return graph_from_csr_impl(ctx, n, n, 0, indptr, indices, nnz, values, shift, scale, out);
+  return graph_from_csr_impl(ctx, n, n, 0, indptr, indices, 8, nnz, values, shift, scale, out);
+}
+
+int kpm_graph_from_csr32(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
+                         const int32_t *indices, int64_t nnz, const double *values,
+                         double shift, double scale, kpm_graph **out) {
+  return graph_from_csr_impl(ctx, n, n, 0, indptr, indices, 4, nnz, values, shift, scale, out);
 }
 
 int kpm_graph_from_csr_part(kpm_ctx *ctx, int64_t n_global, int64_t row_lo, int64_t n_local,
@@ -603,7 +617,7 @@ int kpm_graph_from_csr_part(kpm_ctx *ctx, int64_t n_global, int64_t row_lo, int6
                             kpm_graph **out) {
   KPM_CHECK_ARG(row_lo >= 0 && n_local >= 0 && row_lo + n_local <= n_global,
                 "bad partition rows");
-  return graph_from_csr_impl(ctx, n_local, n_global, row_lo, indptr, indices, nnz, values,
+  return graph_from_csr_impl(ctx, n_local, n_global, row_lo, indptr, indices, 8, nnz, values,
                              shift, scale, out);
 }
 
@@ -618,8 +632,8 @@ int kpm_graph_set_dinv(kpm_graph *g, const double *dinv_global) {
 }
 
 static int graph_from_csr_impl(kpm_ctx *ctx, int64_t n, int64_t n_cols, int64_t row0,
-                               const int64_t *indptr, const int64_t *indices, int64_t nnz,
-                               const double *values, double shift, double scale,
+                               const int64_t *indptr, const void *indices, int idx_bytes,
+                               int64_t nnz, const double *values, double shift, double scale,
                                kpm_graph **out) {
   KPM_CHECK_ARG(ctx && out && n >= 0 && nnz >= 0 && indptr, "bad arguments");
   KPM_CHECK_ARG(nnz == 0 || indices, "indices is NULL");
@@ -660,14 +674,22 @@ static int graph_from_csr_impl(kpm_ctx *ctx, int64_t n, int64_t n_cols, int64_t 
   }
   if (nnz > 0) {
     DevBuf ti;
-    const void *di;
-    int rc = stage_in(st, indices, sizeof(int64_t) * nnz, ti, &di);
-    if (rc != KPM_OK) return fail(rc);
+    const void *di = nullptr;
+    if (idx_bytes == 8) {
+      int rc = stage_in(st, indices, sizeof(int64_t) * nnz, ti, &di);
+      if (rc != KPM_OK) return fail(rc);
+    } else {
+      e = cudaMemcpyAsync(g->col_idx, indices, sizeof(int32_t) * nnz, cudaMemcpyDefault, st);
+      if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); return fail(KPM_ECUDA); }
+    }
     int *bad = nullptr;
     cudaMalloc(&bad, sizeof(int));
     cudaMemsetAsync(bad, 0, sizeof(int), st);
-    idx64_to_32<<<grid_for(nnz), 256, 0, st>>>((const int64_t *)di, nnz, n_cols, g->col_idx,
-                                               bad);
+    if (idx_bytes == 8)
+      idx64_to_32<<<grid_for(nnz), 256, 0, st>>>((const int64_t *)di, nnz, n_cols, g->col_idx,
+                                                 bad);
+    else
+      idx32_check<<<grid_for(nnz), 256, 0, st>>>(g->col_idx, nnz, n_cols, bad);
     int hbad = 0;
     cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
     e = cudaStreamSynchronize(st);
@@ -679,6 +701,47 @@ static int graph_from_csr_impl(kpm_ctx *ctx, int64_t n, int64_t n_cols, int64_t 
       if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); return fail(KPM_ECUDA); }
     }
   }
+  int rc = finish_graph(g);
+  if (rc != KPM_OK) return fail(rc);
+  *out = g;
+  return KPM_OK;
+}
+
+int kpm_graph_replicate(kpm_graph *src, kpm_ctx *ctx, kpm_graph **out) {
+  KPM_CHECK_ARG(src && ctx && out, "bad arguments");
+  KPM_CHECK_ARG(src->row0 == 0 && src->n_global == src->n && !src->dinv_all,
+                "row-partition graphs are not replicated");
+  // the source's stream has built the arrays; the copies run on ctx's stream
+  KPM_CUDA(cudaSetDevice(src->ctx->device));
+  KPM_CUDA(cudaStreamSynchronize(src->ctx->stream));
+  KPM_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int64_t n = src->n, nnz = src->nnz;
+  kpm_graph *g = new kpm_graph();
+  g->ctx = ctx;
+  g->n = n;
+  g->nnz = nnz;
+  g->shift = src->shift;
+  g->scale = src->scale;
+  g->n_global = n;
+  auto fail = [&](int rc) { kpm_graph_free(g); return rc; };
+  if (cudaMalloc(&g->row_ptr, sizeof(int64_t) * (n + 1)) != cudaSuccess ||
+      cudaMalloc(&g->col_idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1)) != cudaSuccess ||
+      cudaMalloc(&g->dinv, sizeof(double) * (n > 0 ? n : 1)) != cudaSuccess ||
+      (src->values &&
+       cudaMalloc(&g->values, sizeof(double) * (nnz > 0 ? nnz : 1)) != cudaSuccess)) {
+    set_error("graph allocation failed");
+    return fail(KPM_ENOMEM);
+  }
+  const int sd = src->ctx->device, dd = ctx->device;
+  cudaError_t e = cudaMemcpyPeerAsync(g->row_ptr, dd, src->row_ptr, sd,
+                                      sizeof(int64_t) * (n + 1), st);
+  if (e == cudaSuccess && nnz > 0)
+    e = cudaMemcpyPeerAsync(g->col_idx, dd, src->col_idx, sd, sizeof(int32_t) * nnz, st);
+  if (e == cudaSuccess && nnz > 0 && src->values)
+    e = cudaMemcpyPeerAsync(g->values, dd, src->values, sd, sizeof(double) * nnz, st);
+  if (e != cudaSuccess) { set_error("%s", cudaGetErrorString(e)); return fail(KPM_ECUDA); }
+  // d^-1/2 and the schedule are recomputed from row_ptr: bit-identical
   int rc = finish_graph(g);
   if (rc != KPM_OK) return fail(rc);
   *out = g;

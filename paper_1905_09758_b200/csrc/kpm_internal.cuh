@@ -104,6 +104,7 @@ struct kpm_run {
   int32_t mode = 0, m_max = 0, flags = 0;
   int32_t total_steps = 0, done_steps = 0;
   bool have_probes = false;
+  bool finished = false;      // LDOS: kpm_run_result turned the sums into values
   double *z = nullptr;        // probes (DIRECT/LDOS), n x ld
   double *a = nullptr, *b = nullptr;  // recurrence blocks
   double *cur = nullptr, *prev = nullptr;  // T_k (gather source), T_{k-1}

@@ -512,8 +512,7 @@ __device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, doub
         if constexpr (INIT) {
           // kpm.py:144-147: den = einsum(z, z) (same reduction as num[0])
           double *den = const_cast<double *>(p.den);
-          den[i] = num;
-          if (!p.ldos_raw && num == 0.0) atomicMin(p.flag + 1, i);
+          den[i] = num;  // zero mass is checked on the final den (kpm_run_result)
         }
         p.ldos[(size_t)i * p.ldos_stride + p.ldos_col] = num;  // raw num[m, i]
       }
@@ -2385,6 +2384,24 @@ __global__ void rademacher_kernel(int64_t n, int64_t ncols, const uint64_t *__re
   }
 }
 
+// kpm.py:145-147: the first node with zero probe mass (den == 0)
+__global__ void first_zero_kernel(const double *__restrict__ den, int64_t n, int32_t *flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (den[i] == 0.0) atomicMin(flag, (int32_t)i);
+}
+
+// dst += src (raw per-node sums of two probe batches / GPU shards)
+__global__ void add_inplace_kernel(double *__restrict__ dst, const double *__restrict__ src,
+                                   int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __dadd_rn(dst[i], src[i]);
+}
+
+__global__ void or_flag_kernel(int32_t *dst, const int32_t *src) { dst[0] |= src[0]; }
+__global__ void set_i32_kernel(int32_t *dst, int32_t v) { dst[0] = v; }
+
 // kpm.py:148-150: values = (num / den).T, or num * trace_scale (raw); the
 // num array is already node-major (n, M+1).
 __global__ void ldos_finish(double *__restrict__ v, const double *__restrict__ den,
@@ -2594,6 +2611,7 @@ static int run_after_probes(kpm_run *r) {
   r->k_index = 0;
   r->done_steps = 0;
   r->have_probes = true;
+  r->finished = false;
   return KPM_OK;
 }
 
@@ -2739,7 +2757,7 @@ int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
 }
 
 int kpm_run_result(kpm_run *r, double *out, double trace_scale, int64_t *bad_node) {
-  KPM_CHECK_ARG(r && out, "bad arguments");
+  KPM_CHECK_ARG(r && (out || r->mode == KPM_MODE_LDOS), "bad arguments");
   KPM_CHECK_ARG(r->have_probes, "probes not set");
   KPM_CHECK_ARG(r->done_steps == r->total_steps, "run not finished (%d of %d steps)",
                 r->done_steps, r->total_steps);
@@ -2748,24 +2766,29 @@ int kpm_run_result(kpm_run *r, double *out, double trace_scale, int64_t *bad_nod
   int32_t hflag[4];
   KPM_CUDA(cudaMemcpyAsync(hflag, r->flag, sizeof(hflag), cudaMemcpyDeviceToHost, st));
   if (r->mode == KPM_MODE_LDOS) {
+    if (!(r->flags & KPM_LDOS_RAW) && r->g->n > 0 && !r->finished) {
+      set_i32_kernel<<<1, 1, 0, st>>>(r->flag + 1, 0x7fffffff);
+      first_zero_kernel<<<grid_of(r->g->n), 256, 0, st>>>(r->den, r->g->n, r->flag + 1);
+      KPM_CUDA(cudaMemcpyAsync(hflag, r->flag, sizeof(hflag), cudaMemcpyDeviceToHost, st));
+    }
     KPM_CUDA(cudaStreamSynchronize(st));
     if (hflag[0]) {
       set_error("Chebyshev recurrence overflowed; re-estimate the spectral range "
                 "with a larger margin");
       return KPM_ENONFINITE;
     }
-    if (!(r->flags & KPM_LDOS_RAW) && hflag[1] != 0x7fffffff) {
+    if (!(r->flags & KPM_LDOS_RAW) && !r->finished && hflag[1] != 0x7fffffff) {
       if (bad_node) *bad_node = hflag[1];
       set_error("zero probe mass at node %d; its moments are unrecoverable", hflag[1]);
       return KPM_EZEROMASS;
     }
-    if (r->g->n > 0)
+    if (r->g->n > 0 && !r->finished)
       ldos_finish<<<grid_of(r->g->n * (r->m_max + 1)), 256, 0, st>>>(
           r->ldos, r->den, r->g->n, r->m_max + 1, (r->flags & KPM_LDOS_RAW) != 0,
           trace_scale);
     KPM_CUDA(cudaGetLastError());
-    r->have_probes = false;  // the num buffer now holds values
-    if (r->g->n > 0)
+    r->finished = true;  // the num buffer now holds values
+    if (r->g->n > 0 && out)
       KPM_CUDA(cudaMemcpyAsync(out, r->ldos,
                                sizeof(double) * (size_t)r->g->n * (r->m_max + 1),
                                cudaMemcpyDefault, st));
@@ -2775,6 +2798,69 @@ int kpm_run_result(kpm_run *r, double *out, double trace_scale, int64_t *bad_nod
   KPM_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * r->k, r->contrib, sizeof(double) * r->ld,
                              sizeof(double) * r->k, r->m_max + 1, cudaMemcpyDefault, st));
   KPM_CUDA(cudaStreamSynchronize(st));
+  return KPM_OK;
+}
+
+int kpm_run_ldos_values(kpm_run *r, const double **values) {
+  KPM_CHECK_ARG(r && values && r->mode == KPM_MODE_LDOS, "not an LDOS run");
+  *values = r->ldos;
+  return KPM_OK;
+}
+
+int kpm_run_accumulate(kpm_run *dst, kpm_run *src) {
+  KPM_CHECK_ARG(dst && src && dst != src, "bad arguments");
+  KPM_CHECK_ARG(dst->mode == KPM_MODE_LDOS && src->mode == KPM_MODE_LDOS,
+                "accumulate combines LDOS runs");
+  KPM_CHECK_ARG(dst->g->n == src->g->n && dst->m_max == src->m_max,
+                "runs differ in n or m_max");
+  KPM_CHECK_ARG(dst->have_probes && src->have_probes && !dst->finished && !src->finished &&
+                    dst->done_steps == dst->total_steps && src->done_steps == src->total_steps,
+                "both runs must be complete and not yet finished by kpm_run_result");
+  const int64_t n = dst->g->n, cnt = n * (dst->m_max + 1);
+  if (n == 0) return KPM_OK;
+  // src's stream has produced its sums; dst's stream orders the rest
+  KPM_CUDA(cudaSetDevice(src->g->ctx->device));
+  KPM_CUDA(cudaStreamSynchronize(src->g->ctx->stream));
+  KPM_CUDA(cudaSetDevice(dst->g->ctx->device));
+  cudaStream_t st = dst->g->ctx->stream;
+  const bool same = src->g->ctx->device == dst->g->ctx->device;
+  const double *sl = src->ldos, *sd = src->den;
+  const int32_t *sf = src->flag;
+  char *tmp = nullptr;
+  if (!same) {  // stage the peer device's sums (NVLink peer copy) on dst's device
+    const size_t bytes = sizeof(double) * (size_t)(cnt + n) + 16;
+    KPM_CUDA(cudaMallocAsync((void **)&tmp, bytes, st));
+    KPM_CUDA(cudaMemcpyPeerAsync(tmp, dst->g->ctx->device, src->ldos, src->g->ctx->device,
+                                 sizeof(double) * cnt, st));
+    KPM_CUDA(cudaMemcpyPeerAsync(tmp + sizeof(double) * cnt, dst->g->ctx->device, src->den,
+                                 src->g->ctx->device, sizeof(double) * n, st));
+    KPM_CUDA(cudaMemcpyPeerAsync(tmp + sizeof(double) * (cnt + n), dst->g->ctx->device,
+                                 src->flag, src->g->ctx->device, sizeof(int32_t), st));
+    sl = (const double *)tmp;
+    sd = sl + cnt;
+    sf = (const int32_t *)(sd + n);
+  }
+  add_inplace_kernel<<<grid_of(cnt), 256, 0, st>>>(dst->ldos, sl, cnt);
+  add_inplace_kernel<<<grid_of(n), 256, 0, st>>>(dst->den, sd, n);
+  or_flag_kernel<<<1, 1, 0, st>>>(dst->flag, sf);
+  KPM_CUDA(cudaGetLastError());
+  if (tmp) KPM_CUDA(cudaFreeAsync(tmp, st));
+  KPM_CUDA(cudaStreamSynchronize(st));
+  return KPM_OK;
+}
+
+int kpm_run_trim(kpm_run *r) {
+  KPM_CHECK_ARG(r, "run is NULL");
+  KPM_CHECK_ARG(r->done_steps == r->total_steps, "run not complete");
+  KPM_CUDA(cudaSetDevice(r->g->ctx->device));
+  KPM_CUDA(cudaStreamSynchronize(r->g->ctx->stream));
+  double **bufs[] = {&r->a, &r->b, &r->z, &r->partial, &r->hpart, &r->hldos, &r->gpart};
+  for (double **b : bufs) {
+    cudaFree(*b);
+    *b = nullptr;
+  }
+  r->cur = r->prev = nullptr;
+  r->tm_ok = r->tm_tile_ok = false;
   return KPM_OK;
 }
 

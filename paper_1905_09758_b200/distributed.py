@@ -39,6 +39,12 @@ def _allreduce_sum(arr: np.ndarray, group=None) -> np.ndarray:
     return t.numpy()
 
 
+def _backend(group):
+    import torch.distributed as dist
+
+    return dist.get_backend(group)
+
+
 def _world(group):
     import torch.distributed as dist
 
@@ -73,15 +79,54 @@ def dos_moments_sharded(sop, probes, m_max, effective_dim=None, doubling=True,
                        probe_meta=probes.meta())
 
 
+def _device_num_allreduce(sop, sub, m_max, group):
+    """NCCL path: this rank's raw per-node sums land in a CUDA tensor straight
+    from the run's device buffer (D2D) and are summed in place by one
+    all-reduce over NVLink -- no host round trip of the (n, M+1) block."""
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib
+    from .kpm import _device_graph, _ldos_run
+
+    dev = _device_graph(sop)
+    num = torch.zeros((sop.n, m_max + 1), dtype=torch.float64,
+                      device=torch.device("cuda", dev.ctx.device))
+    if sub is not None:
+        run = _ldos_run(sop, sub, m_max, _lib.LDOS_RAW)
+        try:
+            run.result(num.data_ptr(), 1.0)  # synchronous on the library stream
+        finally:
+            run.free()
+    dist.all_reduce(num, op=dist.ReduceOp.SUM, group=group)
+    return num
+
+
 def pdos_moments_sharded(sop, probes, m_max, normalized=True, group=None,
                          num_fn=None) -> ChebMoments:
-    """pdos_moments with probe columns sharded: per-node raw sums all-reduced."""
+    """pdos_moments with probe columns sharded: per-node raw sums all-reduced
+    (NCCL: on the device; gloo: host arrays), then kpm.py:143-151."""
     rank, world = _world(group)
     c0, c1 = shard_range(probes.nz, rank, world)
+    sub = probes.column_slice(c0, c1) if c1 > c0 else None
+    if num_fn is None and world > 1 and _backend(group) == "nccl":
+        t = _device_num_allreduce(sop, sub, m_max, group)
+        if not bool(t.isfinite().all()):
+            raise RecurrenceBlowupError(_BLOWUP)
+        if normalized:
+            den = t[:, 0]
+            zero = (den == 0.0).nonzero()
+            if zero.numel():
+                raise ValueError(f"zero probe mass at node {int(zero[0, 0])}; "
+                                 "its moments are unrecoverable")
+            t = t / den[:, None]  # IEEE division, as numpy's (num / den).T
+        else:
+            t = t * probes.trace_scale
+        return ChebMoments(mode=MODE_PER_NODE, values=t.cpu().numpy(),
+                           scale_map=sop.scale_map, probe_meta=probes.meta())
     if num_fn is None:
         from .kpm import pdos_num as num_fn
-    local = num_fn(sop, probes.column_slice(c0, c1), m_max) if c1 > c0 \
-        else np.zeros((sop.n, m_max + 1))
+    local = num_fn(sop, sub, m_max) if sub is not None else np.zeros((sop.n, m_max + 1))
     num = _allreduce_sum(np.ascontiguousarray(local), group) if world > 1 else local
     if not np.all(np.isfinite(num)):
         raise RecurrenceBlowupError(_BLOWUP)
@@ -95,6 +140,45 @@ def pdos_moments_sharded(sop, probes, m_max, normalized=True, group=None,
         values = num * probes.trace_scale
     return ChebMoments(mode=MODE_PER_NODE, values=np.ascontiguousarray(values),
                        scale_map=sop.scale_map, probe_meta=probes.meta())
+
+
+def broadcast_graph(dev, group=None, src=0, ctx=None):
+    """Replicate a device graph to every rank of an NCCL group: rank `src`
+    holds `dev` (e.g. loaded once from the host), the others pass None; the
+    int64 row_ptr and int32 col_idx go out in two NCCL broadcasts over
+    NVLink/NVSwitch and each rank rebuilds d^-1/2 and its schedule from them
+    (bit-identical).  Replaces N host loads/uploads of the same CSR
+    (the CSR is replicated per GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib
+    from .graph import DeviceGraph
+
+    rank, world = _world(group)
+    if world <= 1:
+        return dev
+    ctx = ctx or (dev.ctx if dev is not None else _lib.Context.get())
+    cuda = torch.device("cuda", ctx.device)
+    meta = torch.zeros(3, dtype=torch.int64, device=cuda)
+    if rank == src:
+        if dev.explicit:
+            raise ValueError("broadcast_graph replicates implicit (unit-weight) graphs")
+        meta[0], meta[1] = dev.n, dev.nnz
+    dist.broadcast(meta, src, group=group)
+    n, nnz = int(meta[0]), int(meta[1])
+    rp = torch.empty(n + 1, dtype=torch.int64, device=cuda)
+    ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=cuda)
+    if rank == src:
+        _lib.check(_lib.load().kpm_graph_export(dev.handle, rp.data_ptr(), ci.data_ptr(),
+                                                None), "graph_export")
+    dist.broadcast(rp, src, group=group)
+    dist.broadcast(ci, src, group=group)
+    torch.cuda.synchronize(cuda)
+    if rank != src:
+        dev = DeviceGraph.from_csr(n, rp.data_ptr(), (ci.data_ptr(), nnz, "int32"), ctx=ctx)
+    del rp, ci
+    return dev
 
 
 # ------------------------------------------------ row-partitioned (§8e) ---

@@ -419,12 +419,17 @@ def parse_graph_file(path, fmt=None, allow_self_loops=False, ctx=None):
 
 
 def load_graph_file(path, fmt=None, allow_self_loops=False, ctx=None):
-    """Same parse, graph left in HBM: (DeviceGraph, node_id_map).  Weighted
-    files are uploaded as an explicit operator of their weights."""
+    """Same parse, graph left in HBM: (DeviceGraph, node_id_map).  A
+    DeviceGraph is the unit-weight graph whose normalized adjacency the
+    kernels form from degrees, so a file whose parsed weights are not all 1
+    -- explicit weights, or a same-direction repeated edge, which build_csr
+    sums to weight 2 (graph.py:145-155) -- raises GraphError; such files go
+    through parse_graph_file + build_operator (explicit values)."""
     dev, g, ids = _ingest(path, fmt, allow_self_loops, ctx)
     if dev is None:
-        if g.is_weighted:
-            raise GraphError("load_graph_file: weighted graphs have no implicit "
+        if not g.unit_weights:
+            raise GraphError("load_graph_file: the parsed graph has non-unit edge weights "
+                             "(explicit weights or repeated edges), which have no implicit "
                              "normalized-adjacency device form; use parse_graph_file")
         dev = DeviceGraph.from_csr(g.n, g.row_ptr, g.col_idx, ctx=ctx)
     return dev, ids

@@ -207,16 +207,27 @@ class DeviceGraph:
     @classmethod
     def from_csr(cls, n, indptr, indices, values=None, shift=0.0, scale=1.0,
                  ctx=None) -> "DeviceGraph":
-        """Upload an explicit CSR; values None = implicit normalized adjacency."""
+        """Upload an explicit CSR; values None = implicit normalized adjacency.
+        int32 `indices` go to the device as they are (no widening copy); a
+        device CSR is passed as addresses: indptr an int, indices a tuple
+        (address, nnz, "int32" | "int64")."""
         ctx = ctx or _lib.Context.get()
-        indptr = _as_i64(indptr)
-        indices = _as_i64(indices)
-        if values is not None:
+        indptr = indptr if isinstance(indptr, int) else _as_i64(indptr)
+        if values is not None and not isinstance(values, int):
             values = np.ascontiguousarray(values, dtype=np.float64)
+        lib = _lib.load()
+        if isinstance(indices, tuple):
+            addr, nnz, kind = indices
+            fn = lib.kpm_graph_from_csr32 if kind == "int32" else lib.kpm_graph_from_csr
+        elif isinstance(indices, np.ndarray) and indices.dtype == np.int32:
+            indices = np.ascontiguousarray(indices)
+            addr, nnz, fn = _lib.ptr(indices), indices.shape[0], lib.kpm_graph_from_csr32
+        else:
+            indices = _as_i64(indices)
+            addr, nnz, fn = _lib.ptr(indices), indices.shape[0], lib.kpm_graph_from_csr
         h = ctypes.c_void_p()
-        _lib.check(_lib.load().kpm_graph_from_csr(
-            ctx.handle, int(n), _lib.ptr(indptr), _lib.ptr(indices), int(indices.shape[0]),
-            _lib.ptr(values), float(shift), float(scale), ctypes.byref(h)), "graph_from_csr")
+        _lib.check(fn(ctx.handle, int(n), _lib.ptr(indptr), addr, int(nnz), _lib.ptr(values),
+                      float(shift), float(scale), ctypes.byref(h)), "graph_from_csr")
         return cls(h.value, ctx, explicit=values is not None)
 
     @classmethod
@@ -231,6 +242,21 @@ class DeviceGraph:
             ctx.handle, int(scale), int(edge_factor) << int(scale), int(seed), ta, tab, tabc,
             ctypes.byref(h)), "graph_rmat")
         return cls(h.value, ctx)
+
+    def on(self, ctx) -> "DeviceGraph":
+        """This graph on context `ctx`: itself, or a cached replica copied
+        device to device (peer copy over NVLink for another GPU)."""
+        if ctx is self.ctx:
+            return self
+        reps = self.__dict__.setdefault("_replicas", {})
+        rep = reps.get(id(ctx))
+        if rep is None:
+            h = ctypes.c_void_p()
+            _lib.check(_lib.load().kpm_graph_replicate(self.handle, ctx.handle,
+                                                       ctypes.byref(h)), "graph_replicate")
+            rep = DeviceGraph(h.value, ctx, explicit=self.explicit)
+            reps[id(ctx)] = rep
+        return rep
 
     # ---------------------------------------------------------- exports
     def export(self):
@@ -252,6 +278,8 @@ class DeviceGraph:
         return np.diff(rp).astype(np.float64)
 
     def free(self):
+        for rep in self.__dict__.pop("_replicas", {}).values():
+            rep.free()
         if self._h is not None:
             _lib.load().kpm_graph_free(self._h)
             self._h = None

@@ -158,38 +158,80 @@ class Run:
             pass
 
 
-def _batch_cols(dev, nz, blocks, max_cols=1024):
+def _batch_cols(dev, nz, blocks, max_cols=1024, fixed_bytes=0):
     """Probe columns per batch: all of them when two/three n x ld fp64 blocks
+    (plus `fixed_bytes` of per-run buffers, e.g. the (n, M+1) LDOS result)
     fit in 85% of free HBM, else the largest multiple of 32 that does."""
     free, _ = dev.ctx.mem_info()
     per_col = 8 * max(dev.n, 1) * blocks
-    fit = int(0.85 * free // per_col)
+    fit = int(max(0.85 * free - fixed_bytes, 0) // per_col)
     b = min(nz, max_cols, max(fit, 1))
     if b < nz and b > 32:
         b -= b % 32
     return max(1, b)
 
 
-def dos_contrib(sop, probes: ProbeMatrix, m_max: int, doubling=True, batch=None):
+def _shards(nz, ctxs):
+    """Contiguous balanced column ranges, one per context (empty ones dropped)."""
+    out = []
+    base, extra = divmod(nz, len(ctxs))
+    c0 = 0
+    for i, ctx in enumerate(ctxs):
+        c1 = c0 + base + (1 if i < extra else 0)
+        if c1 > c0:
+            out.append((ctx, c0, c1))
+        c0 = c1
+    return out
+
+
+def _fan_out(jobs):
+    """Run one job per GPU context on its own host thread (the C-ABI calls
+    release the GIL); re-raise the first failure."""
+    if len(jobs) == 1:
+        return [jobs[0]()]
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(len(jobs)) as ex:
+        futs = [ex.submit(j) for j in jobs]
+        return [f.result() for f in futs]
+
+
+def _contexts(dev, threads):
+    """GPU contexts of one call: the graph's own context alone, or the pool of
+    _lib.devices_for(threads) (the graph is replicated where needed)."""
+    devs = _lib.devices_for(threads)
+    return [dev.ctx] if len(devs) <= 1 else _lib.Context.pool(devs)
+
+
+def dos_contrib(sop, probes: ProbeMatrix, m_max: int, doubling=True, batch=None, threads=1):
     """Per-probe contribution matrix contrib[m, j] = z_j^T T_m z_j, shape
-    (m_max+1, nz) (kpm.py:104-108), computed on the device."""
+    (m_max+1, nz) (kpm.py:104-108), computed on the device.  With several
+    GPUs (``threads`` / KPM_DEVICES, see _lib.devices_for) each takes a
+    contiguous column range on a replica of the graph; the columns are
+    independent and their sums fixed by the graph alone, so the result is
+    bitwise that of one GPU and needs no collective."""
     dev = _device_graph(sop)
     nz = probes.nz
     contrib = np.empty((m_max + 1, nz))
     mode = _lib.MODE_DOS_DOUBLING if doubling else _lib.MODE_DOS_DIRECT
-    b = batch or _batch_cols(dev, nz, 2 if doubling else 3)
-    for c0 in range(0, nz, b):
-        c1 = min(nz, c0 + b)
-        sub = probes.column_slice(c0, c1) if (c0, c1) != (0, nz) else probes
-        run = Run(dev, c1 - c0, mode, m_max)
-        try:
-            run.set_probes(sub)
-            run.advance()
-            part = np.empty((m_max + 1, c1 - c0))
-            run.result(part)
-        finally:
-            run.free()
-        contrib[:, c0:c1] = part
+
+    def job(ctx, a0, a1):
+        g = dev.on(ctx)
+        b = batch or _batch_cols(g, a1 - a0, 2 if doubling else 3)
+        for c0 in range(a0, a1, b):
+            c1 = min(a1, c0 + b)
+            sub = probes.column_slice(c0, c1) if (c0, c1) != (0, nz) else probes
+            run = Run(g, c1 - c0, mode, m_max)
+            try:
+                run.set_probes(sub)
+                run.advance()
+                part = np.empty((m_max + 1, c1 - c0))
+                run.result(part)
+            finally:
+                run.free()
+            contrib[:, c0:c1] = part
+
+    _fan_out([lambda c=c, a=a, b=b: job(c, a, b)
+              for c, a, b in _shards(nz, _contexts(dev, threads))])
     return contrib
 
 
@@ -199,14 +241,14 @@ def dos_moments(sop, probes: ProbeMatrix, m_max: int, effective_dim=None, thread
     (kpm.py:92-117).  ``doubling`` (default) evaluates the M+1 moments from
     ceil(M/2) recurrence steps via T_2k = 2T_k^2 - I, T_2k+1 = 2T_k+1 T_k - T_1;
     ``doubling=False`` is the reference's direct estimator z^T T_m z.
-    ``threads`` is accepted for signature parity and ignored."""
-    del threads
+    ``threads`` > 1 spreads the probe columns over that many GPUs
+    (_lib.devices_for)."""
     if m_max < 0:
         raise ValueError("m_max must be >= 0")
     if sop.n != probes.n:
         raise ValueError("probe dimension does not match operator")
     denom = float(effective_dim) if effective_dim is not None else float(sop.n)
-    contrib = dos_contrib(sop, probes, m_max, doubling=doubling, batch=batch)
+    contrib = dos_contrib(sop, probes, m_max, doubling=doubling, batch=batch, threads=threads)
     if not np.all(np.isfinite(contrib)):
         raise RecurrenceBlowupError(_BLOWUP)
     values = contrib.sum(axis=1) * (probes.trace_scale / denom)
@@ -214,14 +256,66 @@ def dos_moments(sop, probes: ProbeMatrix, m_max: int, effective_dim=None, thread
                        probe_meta=probes.meta())
 
 
-def pdos_num(sop, probes: ProbeMatrix, m_max: int) -> np.ndarray:
+def _ldos_run(sop, probes: ProbeMatrix, m_max: int, flags, batch=None, threads=1):
+    """A finished-steps LDOS run holding the per-node sums over ALL probe
+    columns (kpm.py:133-144): each GPU runs its column shard in batches,
+    batches and shards are added into the first run on the device
+    (kpm_run_accumulate: same-GPU add, or a peer copy from another GPU), so
+    the (n, M+1) block never round-trips through the host.  The caller owns
+    the returned Run (result() then free())."""
+    dev = _device_graph(sop)
+    n, nz = sop.n, probes.nz
+    lib = _lib.load()
+    ldos_bytes = 8 * n * (m_max + 1)
+
+    def job(ctx, a0, a1):
+        g = dev.on(ctx)
+        b = batch or _batch_cols(g, a1 - a0, 3, max_cols=1 << 30, fixed_bytes=ldos_bytes)
+        if b < a1 - a0 and not batch:  # an accumulator run sits beside each batch
+            b = _batch_cols(g, a1 - a0, 3, max_cols=1 << 30, fixed_bytes=2 * ldos_bytes)
+        acc = None
+        try:
+            for c0 in range(a0, a1, b):
+                c1 = min(a1, c0 + b)
+                sub = probes.column_slice(c0, c1) if (c0, c1) != (0, nz) else probes
+                run = Run(g, c1 - c0, _lib.MODE_LDOS, m_max, flags)
+                try:
+                    run.set_probes(sub)
+                    run.advance()  # queued: the caller's host work overlaps
+                    if acc is None:
+                        if c1 < a1:  # more batches follow: keep only the sums
+                            _lib.check(lib.kpm_run_trim(run._h), "run_trim")
+                        acc, run = run, None
+                    else:
+                        _lib.check(lib.kpm_run_accumulate(acc._h, run._h), "run_accumulate")
+                finally:
+                    if run is not None:
+                        run.free()
+        except BaseException:
+            if acc is not None:
+                acc.free()
+            raise
+        return acc
+
+    runs = _fan_out([lambda c=c, a=a, b=b: job(c, a, b)
+                     for c, a, b in _shards(nz, _contexts(dev, threads))])
+    try:
+        for other in runs[1:]:
+            _lib.check(lib.kpm_run_accumulate(runs[0]._h, other._h), "run_accumulate")
+    except BaseException:
+        for r in runs:
+            r.free()
+        raise
+    for other in runs[1:]:
+        other.free()
+    return runs[0]
+
+
+def pdos_num(sop, probes: ProbeMatrix, m_max: int, threads=1) -> np.ndarray:
     """Raw per-node sums num[i, m] = sum_j z_ij (T_m z)_ij, shape (n, m_max+1)
     (kpm.py:135-136, node-major) -- the quantity sharded runs all-reduce."""
-    dev = _device_graph(sop)
-    run = Run(dev, probes.nz, _lib.MODE_LDOS, m_max, _lib.LDOS_RAW)
+    run = _ldos_run(sop, probes, m_max, _lib.LDOS_RAW, threads=threads)
     try:
-        run.set_probes(probes)
-        run.advance()
         out = np.empty((sop.n, m_max + 1))
         run.result(out, 1.0)
     finally:
@@ -233,48 +327,19 @@ def pdos_moments(sop, probes: ProbeMatrix, m_max: int, normalized=True, threads=
                  batch=None) -> ChebMoments:
     """Per-node moments c_mk ~= T_m(H)_kk (kpm.py:120-152): the fused kernel
     reduces z (.) T_m z across each row's probe columns every step and writes
-    the (n, M+1) result in place."""
-    del threads
+    the (n, M+1) result in place; probe batches and GPU shards (``threads``)
+    are summed on the device before the normalisation."""
     if m_max < 0:
         raise ValueError("m_max must be >= 0")
     if sop.n != probes.n:
         raise ValueError("probe dimension does not match operator")
-    dev = _device_graph(sop)
-    n, nz = sop.n, probes.nz
-    b = batch or _batch_cols(dev, nz, 3, max_cols=1 << 30)
-    if b >= nz:
-        run = Run(dev, nz, _lib.MODE_LDOS, m_max, 0 if normalized else _lib.LDOS_RAW)
-        try:
-            run.set_probes(probes)
-            run.advance()  # queued; the host pages the result in meanwhile
-            values = np.empty((n, m_max + 1))
-            _lib.prefault(values)
-            run.result(values, probes.trace_scale)
-        finally:
-            run.free()
-    else:
-        # probe batches: raw per-node sums, combined on the host
-        num = np.zeros((n, m_max + 1))
-        for c0 in range(0, nz, b):
-            c1 = min(nz, c0 + b)
-            run = Run(dev, c1 - c0, _lib.MODE_LDOS, m_max, _lib.LDOS_RAW)
-            try:
-                run.set_probes(probes.column_slice(c0, c1))
-                run.advance()
-                part = np.empty((n, m_max + 1))
-                run.result(part, 1.0)
-            finally:
-                run.free()
-            num += part
-        if not np.all(np.isfinite(num)):
-            raise RecurrenceBlowupError(_BLOWUP)
-        if normalized:
-            den = num[:, 0].copy()
-            if np.any(den == 0.0):
-                k = int(np.argmax(den == 0.0))
-                raise ValueError(f"zero probe mass at node {k}; its moments are unrecoverable")
-            values = num / den[:, None]
-        else:
-            values = num * probes.trace_scale
-    return ChebMoments(mode=MODE_PER_NODE, values=np.ascontiguousarray(values),
-                       scale_map=sop.scale_map, probe_meta=probes.meta())
+    run = _ldos_run(sop, probes, m_max, 0 if normalized else _lib.LDOS_RAW, batch=batch,
+                    threads=threads)
+    try:
+        values = np.empty((sop.n, m_max + 1))
+        _lib.prefault(values)
+        run.result(values, probes.trace_scale)
+    finally:
+        run.free()
+    return ChebMoments(mode=MODE_PER_NODE, values=values, scale_map=sop.scale_map,
+                       probe_meta=probes.meta())

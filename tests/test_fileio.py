@@ -116,6 +116,20 @@ def test_load_graph_file_device_resident(name, kpm_ctx):
 
 
 @pytest.mark.gpu
+def test_load_graph_file_rejects_summed_weights(kpm_ctx):
+    """same_dir.txt repeats 0-1 in the same direction: the reference's
+    build_csr sums it to weight 2 with is_weighted=False, which the implicit
+    unit-weight device graph cannot represent -> GraphError, never a silently
+    different operator; parse_graph_file keeps the reference's weights."""
+    from paper_1905_09758_b200.errors import GraphError
+    path = os.path.join(FILES, "same_dir.txt")
+    g, _ = fileio.parse_graph_file(path)
+    assert not g.unit_weights and not g.is_weighted
+    with pytest.raises(GraphError, match="non-unit edge weights"):
+        fileio.load_graph_file(path)
+
+
+@pytest.mark.gpu
 def test_device_parse_large_rmat_text(tmp_path, kpm_ctx):
     """A 2^18-edge R-MAT edge list with comments, CRLF-free mixed whitespace
     and sparse ids: device ingest == host restatement, bit for bit."""

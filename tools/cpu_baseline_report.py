@@ -44,7 +44,7 @@ def run_cfg(cfg, budget):
     kind, prm, P, M = bench.CONFIGS[cfg]
     ldos = cfg == "c2"
     t0 = time.perf_counter()
-    rp, ci, data = bench._host_graph(cfg)
+    rp, ci, data, _ = bench._oracle_graph(cfg)
     t_graph = time.perf_counter() - t0
     n, nnz = rp.shape[0] - 1, ci.shape[0]
     engine = "ref" if orc.ref_spmv() is not None else "c"

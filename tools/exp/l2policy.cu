@@ -1,0 +1,159 @@
+// L2 residency experiment (round 2): can a hot set of gathered rows be kept
+// in the B200's L2 while a cold gather stream and row streams pass through?
+//
+// Synthetic version of the KPM step's access pattern: a 16 GiB block of
+// 512-byte rows (one 64-column fp64 tile); each warp gathers rows, a fraction
+// `p_hot` of them uniform over the first `hot_rows` rows (the "hub" rows), the
+// rest uniform over the whole block; plus a streamed read of a second block
+// (the own-row T_k / T_{k-1} streams).  Variants:
+//   0 plain loads
+//   1 hot rows ld.L2::cache_hint evict_last, everything else evict_first
+//   2 persisting access-policy window over the hot rows (set-aside = max)
+//   3 = 2 + evict_first on cold gathers and streams
+//   4 hot evict_last only (cold/streams plain)
+//   5 TMA-free bulk copies (cp.async.bulk) with the policy of 1
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o l2policy l2policy.cu
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+__device__ __forceinline__ uint64_t mix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) gather(const double2 *__restrict__ blk, int64_t rows,
+                                              int64_t hot_rows, uint32_t p_hot32,
+                                              int64_t n_gathers, const double2 *__restrict__ strm,
+                                              int64_t strm_rows, double *out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t pl, pf;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+  double acc = 0.0;
+  const int64_t per = 8;  // gathers per stream row (~ degree 8 per own row)
+  for (int64_t g0 = warp * per; g0 < n_gathers; g0 += nwarps * per) {
+    // stream: own row of the second block
+    const int64_t srow = (g0 / per) % strm_rows;
+    double2 s;
+    const double2 *sp = strm + srow * 32 + lane;
+    if (V == 1 || V == 3 || V == 5)
+      asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                   : "=d"(s.x), "=d"(s.y) : "l"(sp), "l"(pf));
+    else
+      s = __ldg(sp);
+    acc += s.x + s.y;
+#pragma unroll
+    for (int q = 0; q < per; ++q) {
+      const uint64_t h = mix((uint64_t)(g0 + q));
+      const bool hot = (uint32_t)h < p_hot32;
+      const int64_t row = hot ? (int64_t)((h >> 32) % (uint64_t)hot_rows)
+                              : (int64_t)((h >> 32) % (uint64_t)rows);
+      const double2 *rp = blk + row * 32 + lane;
+      double2 v;
+      if (V == 1 || V == 5) {
+        const uint64_t pol = hot ? pl : pf;
+        asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(v.x), "=d"(v.y) : "l"(rp), "l"(pol));
+      } else if (V == 3) {
+        if (hot) v = __ldg(rp);
+        else
+          asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                       : "=d"(v.x), "=d"(v.y) : "l"(rp), "l"(pf));
+      } else if (V == 4) {
+        if (hot)
+          asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                       : "=d"(v.x), "=d"(v.y) : "l"(rp), "l"(pl));
+        else v = __ldg(rp);
+      } else {
+        v = __ldg(rp);
+      }
+      acc += v.x * v.y;
+    }
+  }
+  if (acc == 123.456) out[0] = acc;
+}
+
+template <int V>
+static float run(const double2 *blk, int64_t rows, int64_t hot_rows, double p_hot, int64_t ng,
+                 const double2 *strm, int64_t srows, double *out, int sms) {
+  const uint32_t p32 = (uint32_t)(p_hot * 4294967296.0);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  gather<V><<<sms * 8, 256>>>(blk, rows, hot_rows, p32, ng / 4, strm, srows, out);  // warm
+  cudaEventRecord(a);
+  gather<V><<<sms * 8, 256>>>(blk, rows, hot_rows, p32, ng, strm, srows, out);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+int main(int argc, char **argv) {
+  const double hot_mb = argc > 1 ? atof(argv[1]) : 64.0;
+  const double p_hot = argc > 2 ? atof(argv[2]) : 0.5;
+  const int only = argc > 3 ? atoi(argv[3]) : -1;
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, 0);
+  printf("L2 %d MB, persisting max %d MB, accessPolicyMaxWindowSize %d MB\n",
+         prop.l2CacheSize >> 20, (int)(prop.persistingL2CacheMaxSize >> 20),
+         prop.accessPolicyMaxWindowSize >> 20);
+  const int64_t row_bytes = 512;
+  const int64_t rows = (16ll << 30) / row_bytes;
+  const int64_t srows = (4ll << 30) / row_bytes;
+  const int64_t hot_rows = (int64_t)(hot_mb * (1 << 20)) / row_bytes;
+  double2 *blk, *strm;
+  double *out;
+  if (cudaMalloc(&blk, rows * row_bytes) || cudaMalloc(&strm, srows * row_bytes) ||
+      cudaMalloc(&out, 8)) {
+    printf("alloc failed\n");
+    return 1;
+  }
+  cudaMemset(blk, 0, rows * row_bytes);
+  cudaMemset(strm, 0, srows * row_bytes);
+  const int64_t ng = 400ll << 20;  // gathers per timed launch (~200 GB)
+  const double bytes = (double)ng * row_bytes * (1.0 + 1.0 / 8);
+  for (int v = 0; v <= 4; ++v) {
+    if (only >= 0 && v != only) continue;
+    cudaStreamAttrValue attr = {};
+    if (v == 2 || v == 3) {
+      size_t setaside = prop.persistingL2CacheMaxSize;
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
+      attr.accessPolicyWindow.base_ptr = blk;
+      size_t win = (size_t)hot_rows * row_bytes;
+      if (win > (size_t)prop.accessPolicyMaxWindowSize) win = prop.accessPolicyMaxWindowSize;
+      attr.accessPolicyWindow.num_bytes = win;
+      attr.accessPolicyWindow.hitRatio = win > setaside ? (float)setaside / win : 1.0f;
+      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(0, cudaStreamAttributeAccessPolicyWindow, &attr);
+    }
+    float ms = 0;
+    switch (v) {
+      case 0: ms = run<0>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 1: ms = run<1>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 2: ms = run<2>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 3: ms = run<3>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 4: ms = run<4>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+    }
+    if (v == 2 || v == 3) {
+      attr.accessPolicyWindow.num_bytes = 0;
+      cudaStreamSetAttribute(0, cudaStreamAttributeAccessPolicyWindow, &attr);
+      cudaCtxResetPersistingL2Cache();
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+    }
+    cudaError_t e = cudaGetLastError();
+    printf("variant %d hot %.0f MB p_hot %.2f: %.2f ms, %.0f GB/s requested, ideal DRAM share %.2f %s\n",
+           v, hot_mb, p_hot, ms, bytes / ms / 1e6, 1.0 - p_hot * 8.0 / 9.0,
+           e ? cudaGetErrorString(e) : "");
+  }
+  return 0;
+}
