@@ -89,14 +89,6 @@ int kpm_init(int device, kpm_ctx **out) {
   c->sm_count = prop.multiProcessorCount;
   c->persist_max = prop.persistingL2CacheMaxSize;
   c->l2_bytes = prop.l2CacheSize;
-  // L2 set-aside for evict_last ("persisting") lines: KPM_PERSIST_MB (-1 = the
-  // device maximum, 0 = none)
-  if (const char *pm = getenv("KPM_PERSIST_MB")) {
-    const double mb = atof(pm);
-    size_t want = mb < 0 ? (size_t)prop.persistingL2CacheMaxSize : (size_t)(mb * 1048576.0);
-    if (want > (size_t)prop.persistingL2CacheMaxSize) want = prop.persistingL2CacheMaxSize;
-    KPM_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-  }
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete c;

@@ -126,6 +126,7 @@ extern "C" int kpm_ldos_histogram(kpm_ctx *ctx, const double *values, int64_t n,
                                   int32_t m_max, const double *damping, const double *table,
                                   int32_t bins, double *masses, double *norm,
                                   double *min_mass) {
+  kpm::Nvtx nvtx_range_("kpm_ldos_histogram");
   KPM_CHECK_ARG(ctx && values && table && masses && n >= 0 && m_max >= 0 && bins >= 1 &&
                     ld >= m_max + 1,
                 "bad arguments");

@@ -388,12 +388,9 @@ int finish_graph(kpm_graph *g) {
     cudaFree(dmx);
     std::vector<int32_t> order(nch);
     for (int64_t c = 0; c < nch; ++c) order[c] = (int32_t)c;
-    // KPM_CHUNK_ORDER=1 (experiment): row-id order, so warps in flight work
-    // one contiguous id window of the graph
-    const char *eo = getenv("KPM_CHUNK_ORDER");
-    if (!(eo && atoi(eo) == 1))
-      std::stable_sort(order.begin(), order.end(),
-                       [&](int32_t x, int32_t y) { return mx[x] > mx[y]; });
+    // longest row first (row-id order measured slower, profiles/r01_chunk_order_exp.log)
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t x, int32_t y) { return mx[x] > mx[y]; });
     KPM_CUDA(cudaMalloc(&g->chunk_order, sizeof(int32_t) * (nch > 0 ? nch : 1)));
     KPM_CUDA(cudaMemcpy(g->chunk_order, order.data(), sizeof(int32_t) * nch,
                         cudaMemcpyHostToDevice));
@@ -509,6 +506,7 @@ extern "C" {
 int kpm_graph_from_edges(kpm_ctx *ctx, int64_t n, const int64_t *u,
                          const int64_t *v, int64_t m, int keep_loops,
                          kpm_graph **out) {
+  kpm::Nvtx nvtx_range_("kpm_graph_from_edges");
   KPM_CHECK_ARG(ctx && out && n >= 0 && m >= 0, "bad arguments");
   KPM_CHECK_ARG(m == 0 || (u && v), "u/v are NULL");
   KPM_CHECK_ARG(n < (int64_t(1) << 31), "n must be < 2^31 (int32 col_idx)");
@@ -544,6 +542,7 @@ int kpm_graph_from_edges(kpm_ctx *ctx, int64_t n, const int64_t *u,
 
 int kpm_graph_rmat(kpm_ctx *ctx, int scale, int64_t n_edges, uint64_t seed,
                    uint32_t ta, uint32_t tab, uint32_t tabc, kpm_graph **out) {
+  kpm::Nvtx nvtx_range_("kpm_graph_rmat");
   KPM_CHECK_ARG(ctx && out && scale >= 1 && scale <= 30 && n_edges >= 0,
                 "bad arguments");
   KPM_CUDA(cudaSetDevice(ctx->device));
@@ -635,6 +634,7 @@ static int graph_from_csr_impl(kpm_ctx *ctx, int64_t n, int64_t n_cols, int64_t 
                                const int64_t *indptr, const void *indices, int idx_bytes,
                                int64_t nnz, const double *values, double shift, double scale,
                                kpm_graph **out) {
+  kpm::Nvtx nvtx_range_("kpm_graph_from_csr");
   KPM_CHECK_ARG(ctx && out && n >= 0 && nnz >= 0 && indptr, "bad arguments");
   KPM_CHECK_ARG(nnz == 0 || indices, "indices is NULL");
   KPM_CHECK_ARG(n < (int64_t(1) << 31), "n must be < 2^31 (int32 col_idx)");
@@ -708,6 +708,7 @@ static int graph_from_csr_impl(kpm_ctx *ctx, int64_t n, int64_t n_cols, int64_t 
 }
 
 int kpm_graph_replicate(kpm_graph *src, kpm_ctx *ctx, kpm_graph **out) {
+  kpm::Nvtx nvtx_range_("kpm_graph_replicate");
   KPM_CHECK_ARG(src && ctx && out, "bad arguments");
   KPM_CHECK_ARG(src->row0 == 0 && src->n_global == src->n && !src->dinv_all,
                 "row-partition graphs are not replicated");

@@ -154,6 +154,7 @@ using namespace kpm;
 extern "C" int kpm_parse_edges(kpm_ctx *ctx, const char *text, int64_t len, int64_t base,
                                int flags, int64_t *nlines_out, int64_t **u_out,
                                int64_t **v_out, int8_t **status_out, int32_t *unusual_out) {
+  kpm::Nvtx nvtx_range_("kpm_parse_edges");
   KPM_CHECK_ARG(ctx && (text || len == 0) && len >= 0 && nlines_out && u_out && v_out &&
                     status_out && unusual_out,
                 "bad arguments");
@@ -236,6 +237,7 @@ extern "C" int kpm_edges_finalize(kpm_ctx *ctx, int64_t nlines, int64_t *u, int6
                                   const int8_t *status, int compact_ids, int64_t n_declared,
                                   int64_t *m_out, int64_t *n_out, int64_t **eu_out,
                                   int64_t **ev_out, int64_t **ids_out, int32_t *info) {
+  kpm::Nvtx nvtx_range_("kpm_edges_finalize");
   KPM_CHECK_ARG(ctx && m_out && n_out && eu_out && ev_out && ids_out && info, "bad arguments");
   KPM_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;

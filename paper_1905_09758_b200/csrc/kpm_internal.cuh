@@ -11,9 +11,20 @@
 
 #include "../../include/kpm.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace kpm {
 
 void set_error(const char *fmt, ...);
+
+// NVTX range per C-ABI phase (graph load, probes, steps, result, ...): shows
+// up in nsys / ncu --nvtx timelines; header-only NVTX v3, no link dependency.
+struct Nvtx {
+  explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx &) = delete;
+  Nvtx &operator=(const Nvtx &) = delete;
+};
 
 #define KPM_CUDA(expr)                                                         \
   do {                                                                         \

@@ -173,6 +173,7 @@ extern "C" int kpm_lanczos(kpm_graph *g, const double *z, int64_t ldz, int64_t k
                            const double *z_norm, double *alphas, double *betas,
                            int32_t *taken, int32_t *exhausted, int32_t *status,
                            double *basis) {
+  kpm::Nvtx nvtx_range_("kpm_lanczos");
   KPM_CHECK_ARG(g && z && z_norm && alphas && betas && taken && exhausted && status,
                 "bad arguments");
   KPM_CHECK_ARG(k >= 1 && steps >= 1 && ldz >= k, "bad sizes");

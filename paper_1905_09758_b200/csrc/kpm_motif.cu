@@ -186,6 +186,7 @@ using namespace kpm;
 extern "C" int kpm_motif_scan(kpm_graph *g, int64_t *open_rows, int8_t *open_ok,
                               int64_t *open_head, int64_t *closed_rows, int8_t *closed_ok,
                               int64_t *closed_head, int64_t *chain_hub, int64_t *chain_mid) {
+  kpm::Nvtx nvtx_range_("kpm_motif_scan");
   KPM_CHECK_ARG(g && open_rows && open_ok && open_head && closed_rows && closed_ok &&
                     closed_head && chain_hub && chain_mid,
                 "bad arguments");

@@ -80,7 +80,6 @@ struct StepParams {
   int tile;                // run the 4-column layout as 64-column gather4 tiles
   int g4;                  // TMA gather4 light path: 0 off, 1 for C <= 2, 2 all layouts
   int lean;                // per-lane async gathers for C <= 2 (light_lean)
-  int g4hint;              // gather4 L2 hint experiment: 0 none, 1 evict_last, 2 evict_first
   int ntiles;              // gather4: light items per chunk = 64-column tiles of one launch
   int fuse_tiles;          // run all 64-column tiles of a step as one launch
   int g4hot;               // hot-ordered gather4 waves with L2 policies (light_g4 HOT)
@@ -275,13 +274,7 @@ __device__ __forceinline__ void ld_vec(const double *p, double (&v)[C]) {
   }
 }
 
-// Gather with an explicit L2 eviction policy (KPM_HOT_POLICY experiments):
-// rows of high-degree vertices are re-gathered many times per step, so they
-// are loaded with evict_last; the rest with evict_first (policy 2) or the
-// default policy (1).
-#ifndef KPM_HOT_POLICY
-#define KPM_HOT_POLICY 0
-#endif
+// L2 eviction policies for gathered rows (the bulk path's hot rows)
 __device__ __forceinline__ uint64_t l2_policy_last() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -292,43 +285,10 @@ __device__ __forceinline__ uint64_t l2_policy_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-template <int C>
-__device__ __forceinline__ void ld_vec_pol(const double *p, double (&v)[C], uint64_t pol) {
-  if constexpr (C == 1) {
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[0]) : "l"(p), "l"(pol));
-  } else if constexpr (C == 2) {
-    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-                 : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
-  } else {
-    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-                 : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
-    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-                 : "=d"(v[2]), "=d"(v[3]) : "l"(p + 2), "l"(pol));
-  }
-}
 
 // plain (coherent) load: Xprev may alias Y
-// T_{k-1} is read exactly once per step (its last use before being
-// overwritten) and T_{k+1} is only read back next step: with KPM_STREAM_HINTS
-// both move with evict-first ("streaming") cache hints so they do not push
-// the re-gathered hub rows of T_k out of L2.
-#ifndef KPM_STREAM_HINTS
-#define KPM_STREAM_HINTS 0
-#endif
 template <int C>
 __device__ __forceinline__ void ld_vec_rw(const double *p, double (&v)[C]) {
-#if KPM_STREAM_HINTS
-  if constexpr (C == 1) {
-    v[0] = __ldcs(p);
-  } else if constexpr (C == 2) {
-    double2 t = __ldcs(reinterpret_cast<const double2 *>(p));
-    v[0] = t.x; v[1] = t.y;
-  } else {
-    double2 t0 = __ldcs(reinterpret_cast<const double2 *>(p));
-    double2 t1 = __ldcs(reinterpret_cast<const double2 *>(p + 2));
-    v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
-  }
-#else
   if constexpr (C == 1) {
     v[0] = *p;
   } else if constexpr (C == 2) {
@@ -339,21 +299,10 @@ __device__ __forceinline__ void ld_vec_rw(const double *p, double (&v)[C]) {
     double2 t1 = *reinterpret_cast<const double2 *>(p + 2);
     v[0] = t0.x; v[1] = t0.y; v[2] = t1.x; v[3] = t1.y;
   }
-#endif
 }
 
 template <int C>
 __device__ __forceinline__ void st_vec(double *p, const double (&v)[C]) {
-#if KPM_STREAM_HINTS
-  if constexpr (C == 1) {
-    __stcs(p, v[0]);
-  } else if constexpr (C == 2) {
-    __stcs(reinterpret_cast<double2 *>(p), make_double2(v[0], v[1]));
-  } else {
-    __stcs(reinterpret_cast<double2 *>(p), make_double2(v[0], v[1]));
-    __stcs(reinterpret_cast<double2 *>(p + 2), make_double2(v[2], v[3]));
-  }
-#else
   if constexpr (C == 1) {
     *p = v[0];
   } else if constexpr (C == 2) {
@@ -362,7 +311,6 @@ __device__ __forceinline__ void st_vec(double *p, const double (&v)[C]) {
     *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
     *reinterpret_cast<double2 *>(p + 2) = make_double2(v[2], v[3]);
   }
-#endif
 }
 
 __device__ __forceinline__ double warp_sum_fixed(double x) {
@@ -424,9 +372,6 @@ __device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, doub
             } else {
               const double dj = __ldg(p.dinv + jl);
               hl = __dmul_rn(di, dj);
-#if KPM_HOT_POLICY
-              if (dj <= p.hot_dinv) jl |= (int)0x80000000;
-#endif
             }
           }
           for (int q = 0; q < cnt; q += U) {
@@ -436,19 +381,7 @@ __device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, doub
               const int j = __shfl_sync(0xffffffffu, jl, (q + u) & 31);
 #pragma unroll
               for (int c = 0; c < C; ++c) v[u][c] = 0.0;
-              if (q + u < cnt && active) {
-#if KPM_HOT_POLICY
-                const double *src = gather_row(p, (uint32_t)j & 0x7fffffffu) + c0;
-#if KPM_HOT_POLICY == 2
-                ld_vec_pol<C>(src, v[u], j < 0 ? l2_policy_last() : l2_policy_first());
-#else
-                if (j < 0) ld_vec_pol<C>(src, v[u], l2_policy_last());
-                else ld_vec<C>(src, v[u]);
-#endif
-#else
-                ld_vec<C>(gather_row(p, (uint32_t)j) + c0, v[u]);
-#endif
-              }
+              if (q + u < cnt && active) ld_vec<C>(gather_row(p, (uint32_t)j) + c0, v[u]);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -584,9 +517,6 @@ __device__ __forceinline__ void stream_finish_row(const StepParams &p, int row, 
 #ifndef KPM_FAST_MINC
 #define KPM_FAST_MINC 1  // smallest column layout that uses the full-wave fast path
 #endif
-#ifndef KPM_STREAM_LA
-#define KPM_STREAM_LA 0
-#endif
 // Light chunk as ONE stream of nonzeros (single column tile, ld <= 32*C):
 // neighbour ids / weights are fetched 32 at a time across row boundaries and
 // U gathers stay in flight continuously, so short rows no longer serialise on
@@ -635,11 +565,8 @@ __device__ __forceinline__ void light_stream(const StepParams &p, int chunk, dou
   int64_t rend = rp(row + 1);
   double di = 0.0;
   if constexpr (!EXPL) di = __shfl_sync(0xffffffffu, wdi, row - wb);
-  // own operands of the current row; with KPM_STREAM_LA also of row+1
+  // own operands of the current row
   double xo[C], pv[C], zv[C];
-#if KPM_STREAM_LA
-  double nxo[C], npv[C], nzv[C];
-#endif
   auto own = [&](int r, double (&a)[C], double (&b)[C], double (&cz)[C]) {
 #pragma unroll
     for (int c = 0; c < C; ++c) a[c] = b[c] = cz[c] = 0.0;
@@ -651,9 +578,6 @@ __device__ __forceinline__ void light_stream(const StepParams &p, int chunk, dou
     }
   };
   own(row, xo, pv, zv);
-#if KPM_STREAM_LA
-  own(row + 1, nxo, npv, nzv);
-#endif
   double acc[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) acc[c] = 0.0;
@@ -669,17 +593,7 @@ __device__ __forceinline__ void light_stream(const StepParams &p, int chunk, dou
       if constexpr (!EXPL) di = __shfl_sync(0xffffffffu, wdi, row - wb);
 #pragma unroll
       for (int c = 0; c < C; ++c) acc[c] = 0.0;
-#if KPM_STREAM_LA
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        xo[c] = nxo[c];
-        pv[c] = npv[c];
-        zv[c] = nzv[c];
-      }
-      own(row + 1, nxo, npv, nzv);
-#else
       own(row, xo, pv, zv);
-#endif
     }
   };
   advance(K0);  // leading empty rows
@@ -1439,12 +1353,6 @@ __global__ void __launch_bounds__(256, KPM_LEAN_MINB) kpm_step_lean_kernel(const
 #ifndef KPM_G4_THREADS
 #define KPM_G4_THREADS 256
 #endif
-#ifndef KPM_G4_FMA
-#define KPM_G4_FMA 0
-#endif
-#ifndef KPM_G4_SEG
-#define KPM_G4_SEG 0  // row-segment consume loop for waves that span rows
-#endif
 template <int C>
 struct G4Tune {  // neighbours per wave, waves in flight, resident 256-thread CTAs
   static constexpr int wave = C == 1 ? KPM_G4_WAVE1 : (C == 2 ? KPM_G4_WAVE2 : 4);
@@ -1610,17 +1518,9 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
         asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(j[4 * q]), "=r"(j[4 * q + 1]), "=r"(j[4 * q + 2]), "=r"(j[4 * q + 3])
                      : "r"(ca + 16 * q));
-#if KPM_G4_SEG
-      if (cnt < WAVE) {
-#pragma unroll
-        for (int k = 1; k < WAVE; ++k)
-          if (k >= cnt) j[k] = j[0];  // a valid row; its bytes land unused
-      }
-#else
 #pragma unroll
       for (int k = 1; k < WAVE; ++k)
         if (k >= cnt) j[k] = j[0];  // a valid row; its bytes land unused
-#endif
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                    "r"((uint32_t)WAVE * rbytes)
                    : "memory");
@@ -1641,16 +1541,6 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
             tma_gather4(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
                         j[4 * q + 2], j[4 * q + 3], bar);
         }
-      } else if (p.g4hint) {
-        uint64_t pol;
-        if (p.g4hint == 1)
-          asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-        else
-          asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-#pragma unroll
-        for (int q = 0; q < WAVE / 4; ++q)
-          tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
-                           j[4 * q + 2], j[4 * q + 3], bar, pol);
       } else {
 #pragma unroll
         for (int q = 0; q < WAVE / 4; ++q)
@@ -1772,32 +1662,17 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       else h = __dmul_rn(di, wv);  // (1*dinv_i)*dinv_j, operators.py:110
 #pragma unroll
       for (int c = 0; c < C; ++c)
-#if KPM_G4_FMA  // experiment: fused multiply-add (not the reference's rounding)
-        acc[c] = __fma_rn(h, v[c], acc[c]);
-#else
         acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[c]));
-#endif
     };
     if (cnt == WAVE && e0 + WAVE <= rend) {
 #pragma unroll
       for (int k = 0; k < WAVE; ++k) add_one(k);
       advance(e0 + WAVE);
     } else {
-#if KPM_G4_SEG
-      // row segments of the wave: the neighbours of one row are added without
-      // per-neighbour row-end checks; advance() then closes the row (and any
-      // empty rows after it)
-      for (int k = 0; k < cnt;) {
-        const int seg = min(cnt, (int)(rend - e0));
-        for (; k < seg; ++k) add_one(k);
-        advance(e0 + k);
-      }
-#else
       for (int k = 0; k < cnt; ++k) {
         add_one(k);
         advance(e0 + k + 1);
       }
-#endif
     }
     __syncwarp();  // the whole warp is done with the slot and its weights
     if (w + D < nw) {
@@ -2273,8 +2148,6 @@ static StepParams base_params(const kpm_run *r) {
   if (const char *e = getenv("KPM_G4")) p.g4 = atoi(e);
   p.lean = 1;  // per-lane async gathers for the 1- and 2-column layouts (KPM_LEAN=0: off)
   if (const char *e = getenv("KPM_LEAN")) p.lean = atoi(e);
-  p.g4hint = 0;
-  if (const char *e = getenv("KPM_G4_HINT")) p.g4hint = atoi(e);
   p.ntiles = 1;
   p.fuse_tiles = 1;  // 64-column tiles of one step in one launch (KPM_FUSE_TILES=0: per tile)
   if (const char *e = getenv("KPM_FUSE_TILES")) p.fuse_tiles = atoi(e);
@@ -2616,6 +2489,7 @@ static int run_after_probes(kpm_run *r) {
 }
 
 int kpm_run_set_probes(kpm_run *r, const double *z, int64_t ldz) {
+  kpm::Nvtx nvtx_range_("kpm_run_set_probes");
   KPM_CHECK_ARG(r && (z || r->g->n == 0), "bad arguments");
   KPM_CHECK_ARG(ldz >= r->k, "ldz < k");
   KPM_CUDA(cudaSetDevice(r->g->ctx->device));
@@ -2627,6 +2501,7 @@ int kpm_run_set_probes(kpm_run *r, const double *z, int64_t ldz) {
 }
 
 int kpm_run_set_rademacher(kpm_run *r, const uint64_t *keys) {
+  kpm::Nvtx nvtx_range_("kpm_run_set_rademacher");
   KPM_CHECK_ARG(r && keys, "bad arguments");
   KPM_CUDA(cudaSetDevice(r->g->ctx->device));
   cudaStream_t st = r->g->ctx->stream;
@@ -2673,6 +2548,7 @@ int kpm_run_set_partition(kpm_run *r, int nparts, const int64_t *part_lo, int me
 }
 
 int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
+  kpm::Nvtx nvtx_range_("kpm_run_advance");
   KPM_CHECK_ARG(r, "run is NULL");
   KPM_CHECK_ARG(r->have_probes, "probes not set");
   cudaStream_t st = r->g->ctx->stream;
@@ -2705,6 +2581,28 @@ int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
     if (trace_path && r->done_steps == trace_step && trace_items > 0) {
       KPM_CUDA(cudaMallocAsync(&p.trace, sizeof(unsigned long long) * 3 * trace_items, st));
       p.fuse_tiles = 0;  // the trace layout is one item per chunk
+    }
+    // KPM_WINDOW_MB (experiment): persisting L2 access-policy window over the
+    // first rows of the gathered block T_k (the highest-degree rows when the
+    // graph is degree-relabelled)
+    static const double window_mb = getenv("KPM_WINDOW_MB") ? atof(getenv("KPM_WINDOW_MB")) : 0.0;
+    if (window_mb > 0.0) {
+      size_t bytes = (size_t)(window_mb * 1048576.0);
+      const size_t blk = sizeof(double) * (size_t)r->g->n * r->ld;
+      if (bytes > blk) bytes = blk;
+      static bool limit_set = false;
+      if (!limit_set) {
+        KPM_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, r->g->ctx->persist_max));
+        limit_set = true;
+      }
+      cudaStreamAttrValue attr = {};
+      attr.accessPolicyWindow.base_ptr = r->cur;
+      attr.accessPolicyWindow.num_bytes = bytes;
+      attr.accessPolicyWindow.hitRatio =
+          bytes > r->g->ctx->persist_max ? (float)r->g->ctx->persist_max / (float)bytes : 1.0f;
+      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      KPM_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr));
     }
     KPM_CUDA(launch_step(r, p, false, first, st));
     if (p.trace) {
@@ -2757,6 +2655,7 @@ int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
 }
 
 int kpm_run_result(kpm_run *r, double *out, double trace_scale, int64_t *bad_node) {
+  kpm::Nvtx nvtx_range_("kpm_run_result");
   KPM_CHECK_ARG(r && (out || r->mode == KPM_MODE_LDOS), "bad arguments");
   KPM_CHECK_ARG(r->have_probes, "probes not set");
   KPM_CHECK_ARG(r->done_steps == r->total_steps, "run not finished (%d of %d steps)",
@@ -2808,6 +2707,7 @@ int kpm_run_ldos_values(kpm_run *r, const double **values) {
 }
 
 int kpm_run_accumulate(kpm_run *dst, kpm_run *src) {
+  kpm::Nvtx nvtx_range_("kpm_run_accumulate");
   KPM_CHECK_ARG(dst && src && dst != src, "bad arguments");
   KPM_CHECK_ARG(dst->mode == KPM_MODE_LDOS && src->mode == KPM_MODE_LDOS,
                 "accumulate combines LDOS runs");
@@ -2957,6 +2857,7 @@ int kpm_probes_rademacher(kpm_ctx *ctx, int64_t n, int64_t ncols, const uint64_t
 int kpm_csr_matvec(kpm_ctx *ctx, int64_t n_rows, const int64_t *indptr,
                    const int64_t *indices, const double *data, int64_t nnz,
                    const double *x, int64_t n_x_rows, int64_t k, double *out) {
+  kpm::Nvtx nvtx_range_("kpm_csr_matvec");
   KPM_CHECK_ARG(ctx && n_rows >= 0 && nnz >= 0 && k >= 0 && n_x_rows >= 0, "bad arguments");
   KPM_CHECK_ARG(indptr && (nnz == 0 || (indices && data)), "NULL CSR arrays");
   if (n_rows == 0 || k == 0) return KPM_OK;
@@ -2989,6 +2890,7 @@ int kpm_csr_matvec(kpm_ctx *ctx, int64_t n_rows, const int64_t *indptr,
 int kpm_filter_probes(kpm_ctx *ctx, int64_t n, int64_t k, double *z, int64_t ldz,
                       int64_t n_groups, const int64_t *group_ptr, const int64_t *vec_ptr,
                       const int64_t *vec_idx, const double *vec_val) {
+  kpm::Nvtx nvtx_range_("kpm_filter_probes");
   KPM_CHECK_ARG(ctx && z && n >= 0 && k >= 0 && ldz >= k && n_groups >= 0, "bad arguments");
   if (n_groups == 0 || k == 0 || n == 0) return KPM_OK;
   KPM_CHECK_ARG(group_ptr && vec_ptr && vec_idx && vec_val, "NULL vector arrays");

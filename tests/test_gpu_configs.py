@@ -35,59 +35,73 @@ def _sop(dev):
     return kp.rescale_operator(kp.NormalizedAdjacencyOperator(dev), (-1.0, 1.0))
 
 
-# SURVEY §8c subset parity: C3 4 probes x all 500 moments, C5 2 probes x the
-# first 100 moments against the oracle recurrence.  The oracle needs ~15 min
-# (C3) / ~6 min (C5) on 16 host cores, so the default suite runs the same
-# comparison over a moment prefix; KPM_FULL_SUBSET=1 runs the full lengths
-# (profiles/r01_subset_parity.log).
-_FULL = os.environ.get("KPM_FULL_SUBSET") == "1"
 _THREADS = len(os.sched_getaffinity(0))
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
-def _host_ram_gb():
-    return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
+def _fixture(cfg):
+    """tests/golden/config_<cfg>.npz/.json: written by the reference's code
+    (tests/golden/make_config_golden.py)."""
+    with np.load(os.path.join(GOLDEN, f"config_{cfg}.npz")) as f:
+        arrs = {k: f[k] for k in f.files}
+    with open(os.path.join(GOLDEN, f"config_{cfg}.json")) as f:
+        import json
+        return arrs, json.load(f)
 
 
-def _subset_parity(oracle, dev, probes, m_max):
-    """GPU per-probe contributions (production doubling path, and direct)
-    vs the oracle's sequential recurrence on the same CSR and probe columns."""
-    rp, ci, dinv = dev.export()
-    ci = ci.astype(np.int64)
-    data = oracle.normadj_values(rp, ci, dinv)
-    want = oracle.c_dos_contrib(rp, ci, data, probes.columns, m_max, threads=_THREADS)
-    del ci, data
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _global_hist(values, bins=50):
+    """histogram_from_moments on a global moment vector of the normalized
+    adjacency (scale map identity)."""
+    mom = kp.ChebMoments(mode="global", values=values, scale_map=kp.ScaleMap(0.0, 1.0),
+                         probe_meta={})
+    return kp.histogram_from_moments(mom, bins=bins).masses
+
+
+def _subset_vs_fixture(cfg, scale, seed, family):
+    """SURVEY §8c subset parity at the FULL moment length: the device CSR
+    (row_ptr SHA) and the per-probe contributions of the fixture's probe
+    columns (production doubling path and the direct estimator) against the
+    reference's recurrence; the subset's finished moments and their damped
+    histogram (L1 <= 1e-6)."""
+    ref, meta = _fixture(cfg)
+    dev = kp.DeviceGraph.rmat(scale, 16, seed)
+    assert (dev.n, dev.nnz) == (meta["n"], meta["nnz"])
+    rp, _, _ = dev.export()
+    assert _sha(rp) == meta["row_ptr_sha"]
+    cols = ref[f"{cfg}/cols"]
+    want = ref[f"{cfg}/contrib"]
+    m_max = want.shape[0] - 1
+    probes = kp.make_probes(dev.n, family, "rademacher", seed=seed).column_slice(
+        int(cols[0]), int(cols[-1]) + 1)
     sop = _sop(dev)
     got = kp.dos_contrib(sop, probes, m_max)
     got_direct = kp.dos_contrib(sop, probes, m_max, doubling=False)
     for j in range(want.shape[1]):
         assert _normwise(got[:, j], want[:, j]) <= 1e-9, j
         assert _normwise(got_direct[:, j], want[:, j]) <= 1e-12, j
-    # the finished moments (kpm.py:115) of the subset
-    d_got = got.sum(axis=1) / (probes.nz * dev.n)
+    d_got = got.sum(axis=1) / (probes.nz * dev.n)   # kpm.py:115
     d_want = want.sum(axis=1) / (probes.nz * dev.n)
     assert _normwise(d_got, d_want) <= 1e-9
-    return _normwise(got, want)
+    l1 = np.abs(_global_hist(d_got) - _global_hist(d_want)).sum()
+    assert l1 <= 1e-6
+    print(cfg, "subset", want.shape, "normwise", _normwise(got, want), "direct",
+          _normwise(got_direct, want), "hist L1", l1)
+    dev.free()
 
 
-def test_c3_probe_subset_vs_oracle(oracle, kpm_ctx):
-    """C3: columns 0-3 of the 128-probe family, all 500 moments with
-    KPM_FULL_SUBSET=1 (else the first 30)."""
-    dev = kp.DeviceGraph.rmat(24, 16, 2)
-    probes = kp.make_probes(dev.n, 128, "rademacher", seed=2).column_slice(0, 4)
-    err = _subset_parity(oracle, dev, probes, 500 if _FULL else 30)
-    print("c3 subset normwise", err, "full" if _FULL else "prefix")
+def test_c3_probe_subset_full_length_vs_reference(kpm_ctx):
+    """C3: columns 0-3 of the 128-probe family x all 500 moments."""
+    _subset_vs_fixture("c3", 24, 2, 128)
 
 
-def test_c5_probe_subset_vs_oracle(oracle, kpm_ctx):
-    """C5: columns 0-1 of the 256-probe family, the first 100 moments with
-    KPM_FULL_SUBSET=1 (else the first 6); the oracle holds int64 indices and
-    fp64 values for 2.1e9 nonzeros (~34 GB of host memory)."""
-    if _host_ram_gb() < 96:
-        pytest.skip("needs ~96 GB of host memory for the C5 oracle operator")
-    dev = kp.DeviceGraph.rmat(26, 16, 4)
-    probes = kp.make_probes(dev.n, 256, "rademacher", seed=4).column_slice(0, 2)
-    err = _subset_parity(oracle, dev, probes, 100 if _FULL else 6)
-    print("c5 subset normwise", err, "full" if _FULL else "prefix")
+def test_c5_probe_subset_full_length_vs_reference(kpm_ctx):
+    """C5: columns 0-1 of the 256-probe family x the first 100 moments."""
+    _subset_vs_fixture("c5", 26, 4, 256)
 
 
 def test_c3_rmat24_csr_bitexact_and_probe_subset(oracle, kpm_ctx):
@@ -140,52 +154,73 @@ def test_c3_full_probe_block_properties(kpm_ctx):
     assert h.masses.sum() == pytest.approx(1.0, abs=1e-12)
 
 
-def test_c2_ba1m_ldos_vs_oracle(oracle, kpm_ctx):
-    """C2: BA(1e6, 5, seed 1) (the reference's generator, SHA-pinned), LDOS
-    with 64 Rademacher probes, 100 moments; the oracle per-node sums over the
-    first 12 moments for all 1e6 nodes; global consistency over all 100."""
+def test_c2_ba1m_ldos_full_vs_oracle_and_reference(oracle, kpm_ctx):
+    """C2 in full: BA(1e6, 5, seed 1), LDOS with 64 Rademacher probes x 100
+    moments -- all 1e6 nodes x 101 moments against the oracle's per-node sums
+    (C restatement of kpm.py:133-148, all host threads), the reference's own
+    kpm_pdos on a 2,032-node sample (tests/golden/config_c2.npz), and the
+    per-node damped histograms of that sample (density.py:63-108, L1 <= 1e-6
+    per node) and of the global values."""
     g = kp.preferential_attachment(1_000_000, 5, seed=1)
+    ref, meta = _fixture("c2")
+    assert _sha(g.row_ptr) == meta["row_ptr_sha"]
     mom, sop = kp.kpm_pdos(g, m_max=100, nz=64, probe_kind="rademacher", seed=1)
     assert mom.values.shape == (g.n, 101)
+    nodes = ref["c2/nodes"]
+    assert np.max(np.abs(mom.values[nodes] - ref["c2/rows"])) <= 1e-12
+    assert _normwise(mom.global_values, ref["c2/global_values"]) <= 1e-12
+    hist = kp.pdos_histogram(sop, kp.make_probes(g.n, 64, "rademacher", seed=1), 100,
+                             bins=50, negativity_tol=np.inf)
+    l1 = np.abs(hist.masses[nodes] - ref["c2/hist_rows"]).sum(axis=1)
+    assert l1.max() <= 1e-6, l1.max()
+    lg = np.abs(_global_hist(mom.global_values) - ref["c2/hist_global"]).sum()
+    assert lg <= 1e-6
+    # every node, every moment, against the oracle
     z = kp.make_probes(g.n, 64, "rademacher", seed=1).columns
-    data = oracle.normadj_values(g.row_ptr, g.col_idx)
-    num = oracle.c_ldos_num(g.row_ptr, g.col_idx, data, z, 12, threads=16)
+    data = oracle.normadj_values_c(g.row_ptr, g.col_idx, oracle.dinv_of(g.row_ptr))
+    num = oracle.c_ldos_num(g.row_ptr, g.col_idx, data, z, 100, threads=_THREADS)
     want = (num / num[0]).T
-    assert np.max(np.abs(mom.values[:, :13] - want)) <= 1e-12
+    err = np.max(np.abs(mom.values - want))
+    assert err <= 1e-12, err
     glob = kp.dos_moments(sop, kp.make_probes(g.n, 64, "rademacher", seed=1), 100,
                           doubling=False)
     assert _normwise(mom.global_values, glob.values) <= 1e-9
     assert np.abs(mom.values[:, 0] - 1.0).max() == 0.0
+    print("c2 full: max |err| vs oracle", err, "sample hist L1 max", l1.max(), "global L1", lg)
 
 
-def test_c4_motif_pipeline_vs_oracle(oracle, kpm_ctx):
-    """C4: BA(2e6, 4, 3) + 500k pendant-twin pairs + 100k stars; detection,
-    device deflation of 64 probes, filtered DOS with 300 moments.  The
-    deflation of 4 probe columns is re-done by the oracle's sequential loop
-    (motifs.py:400-403) and their first 20 moments by the oracle recurrence."""
+def test_c4_full_config_vs_reference_pipeline(oracle, kpm_ctx):
+    """C4 in full against the reference's OWN kpm_dos (tests/golden/config_c4):
+    BA(2e6, 4, 3) + 500k pendant-twin pairs + 100k stars; detection, device
+    deflation of all 64 probes, 300 filtered moments, the spike re-inserted
+    50-bin histogram (L1 <= 1e-6); plus the per-probe contributions of the
+    first 4 filtered columns over all 300 moments."""
     from paper_1905_09758_b200 import motifs as M
 
+    ref, meta = _fixture("c4")
     g = kp.testkit.motif_heavy()
-    assert g.n == 3_400_000
+    assert g.n == meta["n"] and _sha(g.row_ptr) == meta["row_ptr_sha"]
+    assert _sha(g.col_idx) == meta["col_idx_sha"]
     res = kp.kpm_dos(g, m_max=300, nz=64, probe_kind="rademacher", seed=3, bins=50,
                      filter_kinds=("open-twin", "closed-twin", "dangling-two-chain"))
-    r = res.adjustment.deflated_dim
-    assert r > 600_000
-    # the bin masses telescope to d_0 (n-r)/n + r/n (re-inserted spikes)
-    d0 = res.moments.values[0]
-    assert abs(res.histogram.masses.sum() - (d0 * (g.n - r) / g.n + r / g.n)) < 1e-9
-    arrays, removed = M.deflation_vectors(res.instances, g.n)
-    assert removed == res.adjustment.removed
-    z = kp.make_probes(g.n, 64, "rademacher", seed=3).columns[:, :4]
-    zf = oracle.project_out(z, arrays)
-    filt = M.project_probes(kp.make_probes(g.n, 64, "rademacher", seed=3).columns, arrays)
-    assert np.max(np.abs(filt[:, :4] - zf)) <= 1e-12
-    data = oracle.normadj_values(g.row_ptr, g.col_idx)
-    want = oracle.c_dos_contrib(g.row_ptr, g.col_idx, data, zf, 20, threads=16)
+    adj = res.adjustment
+    assert adj.deflated_dim == meta["deflated_dim"]
+    assert {str(k): int(c) for k, c in sorted(adj.removed.items())} == meta["removed"]
+    assert len(res.instances) == meta["instances"]
+    assert _normwise(res.moments.values, ref["c4/values"]) <= 1e-9
+    l1 = np.abs(res.histogram.masses - ref["c4/hist_masses"]).sum()
+    assert l1 <= 1e-6, l1
+    # the first 4 filtered columns, all 300 moments
+    arrays, _ = M.deflation_vectors(res.instances, g.n)
+    filt = M.project_probes(kp.make_probes(g.n, 64, "rademacher", seed=3).columns[:, :4].copy(),
+                            arrays)
+    assert np.max(np.abs(filt.sum(axis=0) - ref["c4/filtered4_sum"])) <= 1e-9
     sop = kp.scaled_operator_for(g, "normalized-adjacency")
-    got = kp.dos_contrib(sop, kp.ProbeMatrix(g.n, 4, "rademacher", 3, columns=filt[:, :4]),
-                         20)
-    assert _normwise(got, want) <= 1e-9
+    got = kp.dos_contrib(sop, kp.ProbeMatrix(g.n, 4, "rademacher", 3, columns=filt), 300)
+    for j in range(4):
+        assert _normwise(got[:, j], ref["c4/contrib4"][:, j]) <= 1e-9, j
+    print("c4 full: moments normwise", _normwise(res.moments.values, ref["c4/values"]),
+          "hist L1", l1)
 
 
 def test_c5_rmat26_one_gpu_batch(kpm_ctx):
