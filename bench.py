@@ -61,6 +61,7 @@ CONFIGS = {
     "c4": ("motif", dict(n_ba=2_000_000, m=4, seed=3), 64, 300),
     "c5": ("rmat", dict(scale=26, edge_factor=16, seed=4), 256, 1000),
     "rmat20": ("rmat", dict(scale=20, edge_factor=16, seed=2), 128, 500),
+    "rmat14": ("rmat", dict(scale=14, edge_factor=16, seed=2), 8, 20),  # CPU contract test
 }
 METRIC = "KPM nnz*probes*moments/sec (G/s) and achieved HBM GB/s"
 UNIT = "G nnz*probe*moment/s"
@@ -68,12 +69,24 @@ KERNEL_SOURCES = ("paper_1905_09758_b200/csrc/kpm_step.cu",
                   "paper_1905_09758_b200/csrc/kpm_internal.cuh")
 
 
+def _code_only(src: str) -> str:
+    """C++ source without comments and with whitespace collapsed, so that the
+    hash follows the code, not its commentary."""
+    import re
+
+    src = re.sub(r"/\*.*?\*/", " ", src, flags=re.S)
+    src = re.sub(r"//[^\n]*", " ", src)
+    return " ".join(src.split())
+
+
 def kernel_hash() -> str:
-    """sha256 of the step kernel's sources: keys profiles/traffic.json."""
+    """sha256 of the step kernel's code (comments and whitespace ignored):
+    keys profiles/traffic.json (tests/test_bench_contract.py fails when an
+    entry there was measured on other code)."""
     h = hashlib.sha256()
     for f in KERNEL_SOURCES:
-        with open(os.path.join(REPO, f), "rb") as fh:
-            h.update(fh.read())
+        with open(os.path.join(REPO, f), "r", encoding="utf-8") as fh:
+            h.update(_code_only(fh.read()).encode())
     return h.hexdigest()[:16]
 
 

@@ -11,7 +11,11 @@
 //   2 persisting access-policy window over the hot rows (set-aside = max)
 //   3 = 2 + evict_first on cold gathers and streams
 //   4 hot evict_last only (cold/streams plain)
-//   5 TMA-free bulk copies (cp.async.bulk) with the policy of 1
+//   5 = 1 (reserved)
+//   6 hot plain (evict_normal), cold gathers and streams evict_first, no window
+//   7 hot evict_last, cold gathers evict_first, streams plain
+// Every variant also writes one 512-byte row per 8 gathers (the T_{k+1} stream),
+// with evict_first where the variant streams with evict_first.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o l2policy l2policy.cu
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -43,12 +47,21 @@ __global__ void __launch_bounds__(256) gather(const double2 *__restrict__ blk, i
     const int64_t srow = (g0 / per) % strm_rows;
     double2 s;
     const double2 *sp = strm + srow * 32 + lane;
-    if (V == 1 || V == 3 || V == 5)
+    constexpr bool SF = (V == 1 || V == 3 || V == 5 || V == 6);
+    if (SF)
       asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
                    : "=d"(s.x), "=d"(s.y) : "l"(sp), "l"(pf));
     else
       s = __ldg(sp);
     acc += s.x + s.y;
+    {  // the written stream (second half of the stream block)
+      double2 *wp = const_cast<double2 *>(strm) + (strm_rows + srow) * 32 + lane;
+      if (SF)
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(wp), "d"(s.x),
+                     "d"(s.y), "l"(pf) : "memory");
+      else
+        *wp = s;
+    }
 #pragma unroll
     for (int q = 0; q < per; ++q) {
       const uint64_t h = mix((uint64_t)(g0 + q));
@@ -57,11 +70,11 @@ __global__ void __launch_bounds__(256) gather(const double2 *__restrict__ blk, i
                               : (int64_t)((h >> 32) % (uint64_t)rows);
       const double2 *rp = blk + row * 32 + lane;
       double2 v;
-      if (V == 1 || V == 5) {
+      if (V == 1 || V == 5 || V == 7) {
         const uint64_t pol = hot ? pl : pf;
         asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
                      : "=d"(v.x), "=d"(v.y) : "l"(rp), "l"(pol));
-      } else if (V == 3) {
+      } else if (V == 3 || V == 6) {
         if (hot) v = __ldg(rp);
         else
           asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
@@ -108,20 +121,21 @@ int main(int argc, char **argv) {
          prop.accessPolicyMaxWindowSize >> 20);
   const int64_t row_bytes = 512;
   const int64_t rows = (16ll << 30) / row_bytes;
-  const int64_t srows = (4ll << 30) / row_bytes;
+  const int64_t srows = (4ll << 30) / row_bytes;  // read half; an equal written half follows
   const int64_t hot_rows = (int64_t)(hot_mb * (1 << 20)) / row_bytes;
   double2 *blk, *strm;
   double *out;
-  if (cudaMalloc(&blk, rows * row_bytes) || cudaMalloc(&strm, srows * row_bytes) ||
+  if (cudaMalloc(&blk, rows * row_bytes) || cudaMalloc(&strm, 2 * srows * row_bytes) ||
       cudaMalloc(&out, 8)) {
     printf("alloc failed\n");
     return 1;
   }
   cudaMemset(blk, 0, rows * row_bytes);
-  cudaMemset(strm, 0, srows * row_bytes);
+  cudaMemset(strm, 0, 2 * srows * row_bytes);
   const int64_t ng = 400ll << 20;  // gathers per timed launch (~200 GB)
-  const double bytes = (double)ng * row_bytes * (1.0 + 1.0 / 8);
-  for (int v = 0; v <= 4; ++v) {
+  const double bytes = (double)ng * row_bytes * (1.0 + 2.0 / 8);
+  for (int v = 0; v <= 7; ++v) {
+    if (v == 5) continue;
     if (only >= 0 && v != only) continue;
     cudaStreamAttrValue attr = {};
     if (v == 2 || v == 3) {
@@ -143,6 +157,8 @@ int main(int argc, char **argv) {
       case 2: ms = run<2>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
       case 3: ms = run<3>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
       case 4: ms = run<4>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 6: ms = run<6>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 7: ms = run<7>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
     }
     if (v == 2 || v == 3) {
       attr.accessPolicyWindow.num_bytes = 0;
@@ -152,7 +168,7 @@ int main(int argc, char **argv) {
     }
     cudaError_t e = cudaGetLastError();
     printf("variant %d hot %.0f MB p_hot %.2f: %.2f ms, %.0f GB/s requested, ideal DRAM share %.2f %s\n",
-           v, hot_mb, p_hot, ms, bytes / ms / 1e6, 1.0 - p_hot * 8.0 / 9.0,
+           v, hot_mb, p_hot, ms, bytes / ms / 1e6, 1.0 - p_hot * 8.0 / 10.0,
            e ? cudaGetErrorString(e) : "");
   }
   return 0;
