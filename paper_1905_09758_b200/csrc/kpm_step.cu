@@ -1377,6 +1377,17 @@ struct G4 {
   static_assert(D >= 1 && R >= 1 && (R & (R - 1)) == 0, "gather4 ring shape");
 };
 
+// One elected lane of a converged warp (lane 0): unlike `lane == 0`, ptxas
+// knows a single thread runs the guarded TMA issue, so the uniform-register
+// operands need no waterfall loop.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void tma_gather4_hint(uint32_t dst, const CUtensorMap *tm, int x,
                                                  int j0, int j1, int j2, int j3, uint32_t bar,
                                                  uint64_t pol) {
@@ -1510,7 +1521,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       if (lane < cnt) asm volatile("st.shared.b32 [%0], %1;" ::"r"(ca + posw * 4), "r"(jk) : "memory");
       __syncwarp();
     }
-    if (lane == 0) {
+    if (elect_one()) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads of the slot
       int j[WAVE];
 #pragma unroll
@@ -1518,9 +1529,11 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
         asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(j[4 * q]), "=r"(j[4 * q + 1]), "=r"(j[4 * q + 2]), "=r"(j[4 * q + 3])
                      : "r"(ca + 16 * q));
+      if (cnt < WAVE) {  // the chunk's last wave
 #pragma unroll
-      for (int k = 1; k < WAVE; ++k)
-        if (k >= cnt) j[k] = j[0];  // a valid row; its bytes land unused
+        for (int k = 1; k < WAVE; ++k)
+          if (k >= cnt) j[k] = j[0];  // a valid row; its bytes land unused
+      }
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                    "r"((uint32_t)WAVE * rbytes)
                    : "memory");
@@ -1647,7 +1660,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     const int cnt = min(WAVE, nnz - e0);
     const uint32_t slot = rows_sa + sl * (uint32_t)(L::slot_d * 8) + my_col;
     const uint32_t wslot = HOT ? wv_slot(w) : wv_sa + sl * WAVE * 8;
-    auto add_one = [&](int k) {
+    auto add_h = [&](int k, double h) {
       double v[C];
       if constexpr (HOT) {
         const int pk = __shfl_sync(0xffffffffu, posw, k);
@@ -1655,18 +1668,36 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       } else {
         lds_cols<C>(slot + k * rbytes, v);
       }
-      double wv;
-      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wv) : "r"(wslot + k * 8));
-      double h;
-      if constexpr (EXPL) h = wv;
-      else h = __dmul_rn(di, wv);  // (1*dinv_i)*dinv_j, operators.py:110
 #pragma unroll
       for (int c = 0; c < C; ++c)
         acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[c]));
     };
+    auto add_one = [&](int k) {
+      double wv;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wv) : "r"(wslot + k * 8));
+      if constexpr (EXPL) add_h(k, wv);
+      else add_h(k, __dmul_rn(di, wv));  // (1*dinv_i)*dinv_j, operators.py:110
+    };
     if (cnt == WAVE && e0 + WAVE <= rend) {
+      // the whole wave belongs to one row: each h_ij = dinv_i * dinv_j is
+      // formed once (lane k for neighbour k, the same rounding) and broadcast
+      // in pairs, instead of once per lane and neighbour
+      if constexpr (!EXPL) {
+        if (lane < WAVE) {
+          double wk;
+          asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wk) : "r"(wslot + lane * 8));
+          wk = __dmul_rn(di, wk);  // (1*dinv_i)*dinv_j, operators.py:110
+          asm volatile("st.shared.f64 [%0], %1;" ::"r"(wslot + lane * 8), "d"(wk) : "memory");
+        }
+        __syncwarp();
+      }
 #pragma unroll
-      for (int k = 0; k < WAVE; ++k) add_one(k);
+      for (int k = 0; k < WAVE; k += 2) {
+        double h0, h1;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(h0), "=d"(h1) : "r"(wslot + k * 8));
+        add_h(k, h0);
+        add_h(k + 1, h1);
+      }
       advance(e0 + WAVE);
     } else {
       for (int k = 0; k < cnt; ++k) {
