@@ -171,16 +171,17 @@ __global__ void dinv_kernel(const int64_t *__restrict__ row_ptr, int64_t n,
 // policy picks its "hot" (re-gathered) rows from it.
 __global__ void deg_hist_kernel(const int64_t *__restrict__ row_ptr, int64_t n,
                                 unsigned long long *__restrict__ hist) {
-  __shared__ unsigned long long sh[64];
-  if (threadIdx.x < 64) sh[threadIdx.x] = 0;
+  __shared__ unsigned long long sh[kDegBuckets];
+  for (int b = threadIdx.x; b < kDegBuckets; b += blockDim.x) sh[b] = 0;
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t d = row_ptr[i + 1] - row_ptr[i];
-    if (d > 0) atomicAdd(&sh[63 - __clzll((unsigned long long)d)], 1ull);
+    if (d > 0) atomicAdd(&sh[deg_bucket((unsigned long long)d)], 1ull);
   }
   __syncthreads();
-  if (threadIdx.x < 64 && sh[threadIdx.x]) atomicAdd(hist + threadIdx.x, sh[threadIdx.x]);
+  for (int b = threadIdx.x; b < kDegBuckets; b += blockDim.x)
+    if (sh[b]) atomicAdd(hist + b, sh[b]);
 }
 
 // Chunk c covers rows [start[c], start[c+1]); boundaries split the prefix of
@@ -260,10 +261,10 @@ int finish_graph(kpm_graph *g) {
   KPM_CUDA(cudaFreeAsync(dmax, st));
   {
     unsigned long long *dh = nullptr;
-    KPM_CUDA(cudaMallocAsync(&dh, sizeof(unsigned long long) * 64, st));
-    KPM_CUDA(cudaMemsetAsync(dh, 0, sizeof(unsigned long long) * 64, st));
+    KPM_CUDA(cudaMallocAsync(&dh, sizeof(unsigned long long) * kDegBuckets, st));
+    KPM_CUDA(cudaMemsetAsync(dh, 0, sizeof(unsigned long long) * kDegBuckets, st));
     if (n > 0) deg_hist_kernel<<<grid_for(n), 256, 0, st>>>(g->row_ptr, n, dh);
-    KPM_CUDA(cudaMemcpyAsync(g->deg_log2_hist, dh, sizeof(unsigned long long) * 64,
+    KPM_CUDA(cudaMemcpyAsync(g->deg_hist, dh, sizeof(unsigned long long) * kDegBuckets,
                              cudaMemcpyDeviceToHost, st));
     KPM_CUDA(cudaFreeAsync(dh, st));
   }

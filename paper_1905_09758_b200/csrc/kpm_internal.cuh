@@ -77,6 +77,25 @@ struct kpm_ctx {
 
 // Device CSR: int64 row_ptr, int32 col_idx, fp64 dinv (implicit normalized
 // adjacency) or fp64 values + (shift, scale) (explicit operator).
+// degree buckets of the hot-row rule: 8 per octave (3 mantissa bits)
+static constexpr int kDegBuckets = 512;
+__host__ __device__ inline int deg_bucket(unsigned long long d) {  // d >= 1
+#ifdef __CUDA_ARCH__
+  const int e = 63 - __clzll((long long)d);
+#else
+  int e = 0;
+  for (unsigned long long t = d; t > 1; t >>= 1) ++e;
+#endif
+  const unsigned long long m = e >= 3 ? (d >> (e - 3)) & 7ull : (d << (3 - e)) & 7ull;
+  return 8 * e + (int)m;
+}
+inline double deg_bucket_lo(int b) {
+  const int e = b >> 3, m = b & 7;
+  double lo = 1.0;
+  for (int q = 0; q < e; ++q) lo *= 2.0;
+  return lo * (1.0 + m / 8.0);
+}
+
 struct kpm_graph {
   kpm_ctx *ctx = nullptr;
   int64_t n = 0, nnz = 0, max_degree = 0;
@@ -98,8 +117,9 @@ struct kpm_graph {
   // global).  dinv_all: d^-1/2 of all n_global rows (NULL = dinv, unpartitioned)
   int64_t row0 = 0, n_global = 0;
   double *dinv_all = nullptr;
-  // rows per floor(log2(degree)) bucket (finish_graph): hot-row L2 policy
-  unsigned long long deg_log2_hist[64] = {};
+  // rows per degree bucket, 8 buckets per octave (bucket b holds degrees
+  // [deg_bucket_lo(b), deg_bucket_lo(b + 1)); finish_graph): hot-row L2 policy
+  unsigned long long deg_hist[kDegBuckets] = {};
 };
 
 #define KPM_MAX_PARTS 16

@@ -144,6 +144,12 @@ __device__ __forceinline__ void cp_async_8(uint32_t dst, const void *src) {
 __device__ __forceinline__ void cp_async_4(uint32_t dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
+// streamed operands (read once per step): L2 evict_first
+__device__ __forceinline__ void cp_async_4_first(uint32_t dst, const void *src, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
+               "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -310,6 +316,23 @@ __device__ __forceinline__ void st_vec(double *p, const double (&v)[C]) {
   } else {
     *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
     *reinterpret_cast<double2 *>(p + 2) = make_double2(v[2], v[3]);
+  }
+}
+
+// T_{k+1} rows are written once and next read a whole step later: evict_first
+template <int C>
+__device__ __forceinline__ void st_vec_first(double *p, const double (&v)[C], uint64_t pol) {
+  if constexpr (C == 1) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v[0]), "l"(pol)
+                 : "memory");
+  } else {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v[0]),
+                 "d"(v[1]), "l"(pol)
+                 : "memory");
+    if constexpr (C == 4)
+      asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p + 2), "d"(v[2]),
+                   "d"(v[3]), "l"(pol)
+                   : "memory");
   }
 }
 
@@ -728,12 +751,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 
 // Row epilogue of the bulk path: as stream_finish_row, with the moment
 // products folded into per-lane registers (the lane owns fixed columns).
-template <int C, int MODE, bool EXPL, bool FIRST>
+template <int C, int MODE, bool EXPL, bool FIRST, bool SFIRST = false>
 __device__ __forceinline__ void bulk_finish_row(const StepParams &p, int row, bool active,
                                                 int64_t c0, const double (&acc)[C],
                                                 const double (&xo)[C], const double (&pv)[C],
                                                 const double (&zv)[C], double (&s1)[C],
-                                                double (&s2)[C]) {
+                                                double (&s2)[C], uint64_t pol_first = 0) {
   const int lane = threadIdx.x & 31;
   double lsum = 0.0;
   if (active) {
@@ -754,7 +777,8 @@ __device__ __forceinline__ void bulk_finish_row(const StepParams &p, int row, bo
 #pragma unroll
       for (int c = 0; c < C; ++c) y[c] = __dsub_rn(__dmul_rn(2.0, y[c]), pv[c]);
     }
-    st_vec<C>(p.Y + (size_t)row * p.ld + c0, y);
+    if constexpr (SFIRST) st_vec_first<C>(p.Y + (size_t)row * p.ld + c0, y, pol_first);
+    else st_vec<C>(p.Y + (size_t)row * p.ld + c0, y);
     if constexpr (MODE == MODE_DBL) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
@@ -1069,6 +1093,22 @@ __device__ __forceinline__ void cp_async_cols(uint32_t dst, const double *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
     if constexpr (C == 4)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(src + 2)
+                   : "memory");
+  }
+}
+template <int C>
+__device__ __forceinline__ void cp_async_cols_hint(uint32_t dst, const double *src, uint64_t pol) {
+  if constexpr (C == 1) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(dst),
+                 "l"(src), "l"(pol)
+                 : "memory");
+  } else {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst),
+                 "l"(src), "l"(pol)
+                 : "memory");
+    if constexpr (C == 4)
+      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst + 16),
+                   "l"(src + 2), "l"(pol)
                    : "memory");
   }
 }
@@ -1440,6 +1480,12 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     }
     return;
   }
+  // HOT: everything that is read or written once per step (col ids, own rows,
+  // T_{k+1}, the cold gathers) carries L2 evict_first, so that the hot rows --
+  // gathered with NO hint -- stay resident (tools/exp/l2policy.cu: evict_last
+  // on TMA copies does not hold lines, evict_first on the cold traffic does)
+  uint64_t pol_first = 0;
+  if constexpr (HOT) pol_first = l2_policy_first();
   const uint32_t rows_sa = smem_u32(base);
   const uint32_t wv_sa = rows_sa + L::rows_d * 8;
   const uint32_t col_sa = wv_sa + L::wv_d * 8;
@@ -1470,9 +1516,16 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       const size_t off = (size_t)r * ld + c0;
       const uint32_t dst = own_sa + (uint32_t)(sl * NOP * W + lane * C) * 8;
       int q = 0;
-      if constexpr (EXPL || MODE == MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.X + off);
-      if constexpr (!FIRST) cp_async_cols<C>(dst + (q++) * W * 8, p.Xprev + off);
-      if constexpr (MODE != MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.Z + off);
+      if constexpr (HOT) {
+        // the own row of T_k is also gathered by its neighbours: no hint
+        if constexpr (EXPL || MODE == MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.X + off);
+        if constexpr (!FIRST) cp_async_cols_hint<C>(dst + (q++) * W * 8, p.Xprev + off, pol_first);
+        if constexpr (MODE != MODE_DBL) cp_async_cols_hint<C>(dst + (q++) * W * 8, p.Z + off, pol_first);
+      } else {
+        if constexpr (EXPL || MODE == MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.X + off);
+        if constexpr (!FIRST) cp_async_cols<C>(dst + (q++) * W * 8, p.Xprev + off);
+        if constexpr (MODE != MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.Z + off);
+      }
     }
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(obar + sl))
                  : "memory");
@@ -1493,7 +1546,10 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
   };
   auto issue_col = [&](int w) {
     const int e = w * WAVE + lane;
-    if (lane < WAVE && e < nnz) cp_async_4(col_slot(w) + lane * 4, p.col + K0 + e);
+    if (lane < WAVE && e < nnz) {
+      if constexpr (HOT) cp_async_4_first(col_slot(w) + lane * 4, p.col + K0 + e, pol_first);
+      else cp_async_4(col_slot(w) + lane * 4, p.col + K0 + e);
+    }
   };
   // wave w: rows by gather4 (lane 0), weights by lanes < cnt; the caller then
   // lets lanes < WAVE arrive (noinc) after also issuing col(w + D)
@@ -1539,17 +1595,12 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
                    : "memory");
       const uint32_t dst = rows_sa + sl * (uint32_t)(L::slot_d * 8);
       if constexpr (HOT) {
-        uint64_t pl, pf;
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+        // groups with a hot row: no hint; all-cold groups: evict_first
 #pragma unroll
         for (int q = 0; q < WAVE / 4; ++q) {
-          if (4 * q + 4 <= nh)
+          if (4 * q >= nh)
             tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
-                             j[4 * q + 2], j[4 * q + 3], bar, pl);
-          else if (4 * q >= nh)
-            tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
-                             j[4 * q + 2], j[4 * q + 3], bar, pf);
+                             j[4 * q + 2], j[4 * q + 3], bar, pol_first);
           else
             tma_gather4(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
                         j[4 * q + 2], j[4 * q + 3], bar);
@@ -1634,7 +1685,8 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       if constexpr (!FIRST) lds_cols<C>(a + (q++) * W * 8, pv);
       if constexpr (MODE != MODE_DBL) lds_cols<C>(a + (q++) * W * 8, zv);
     }
-    bulk_finish_row<C, MODE, EXPL, FIRST>(p, r, active, c0, acc, xo, pv, zv, s1, s2);
+    bulk_finish_row<C, MODE, EXPL, FIRST, HOT>(p, r, active, c0, acc, xo, pv, zv, s1, s2,
+                                               pol_first);
     issue_own(r + R);
   };
   auto advance = [&](int64_t kk) {
@@ -1729,7 +1781,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
 }
 
 template <int C, int MODE, bool EXPL, bool FIRST, bool HOT>
-__global__ void __launch_bounds__(256, G4Tune<C>::minb)
+__global__ void __launch_bounds__(KPM_G4_THREADS, G4Tune<C>::minb)
 kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
   using L = G4<C, MODE, EXPL, FIRST>;
   extern __shared__ __align__(128) double sg4[];
@@ -2193,10 +2245,10 @@ static StepParams base_params(const kpm_run *r) {
     if (const char *e = getenv("KPM_HOT_MB")) kHotBytes = atof(e) * 1024 * 1024;
     const double budget = kHotBytes / (8.0 * (double)r->ld);
     double rows = 0.0, hot_deg = 0.0;
-    for (int b = 63; b >= 0; --b) {
-      rows += (double)g->deg_log2_hist[b];
+    for (int b = kDegBuckets - 1; b >= 0; --b) {
+      rows += (double)g->deg_hist[b];
       if (rows > budget) break;
-      hot_deg = std::ldexp(1.0, b);
+      hot_deg = deg_bucket_lo(b);
     }
     if (const char *e = getenv("KPM_HOT_DEGREE")) hot_deg = atof(e);
     if (hot_deg > 0) p.hot_dinv = 1.0 / sqrt(hot_deg);
@@ -2218,10 +2270,10 @@ static StepParams base_params(const kpm_run *r) {
     if (const char *e = getenv("KPM_G4_HOT")) p.g4hot = atoi(e);
     const double budget = hot_bytes / (8.0 * (double)seg);
     double rows = 0.0, hot_deg = 0.0;
-    for (int b = 63; b >= 0; --b) {
-      rows += (double)g->deg_log2_hist[b];
+    for (int b = kDegBuckets - 1; b >= 0; --b) {
+      rows += (double)g->deg_hist[b];
       if (rows > budget) break;
-      hot_deg = std::ldexp(1.0, b);
+      hot_deg = deg_bucket_lo(b);
     }
     if (hot_deg > 0) p.hot_dinv_g4 = 1.0 / sqrt(hot_deg);
   }

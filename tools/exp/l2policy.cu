@@ -14,6 +14,7 @@
 //   5 = 1 (reserved)
 //   6 hot plain (evict_normal), cold gathers and streams evict_first, no window
 //   7 hot evict_last, cold gathers evict_first, streams plain
+//   10-13 the gathers as TMA bulk copies (see gather_tma)
 // Every variant also writes one 512-byte row per 8 gathers (the T_{k+1} stream),
 // with evict_first where the variant streams with evict_first.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o l2policy l2policy.cu
@@ -93,6 +94,109 @@ __global__ void __launch_bounds__(256) gather(const double2 *__restrict__ blk, i
   if (acc == 123.456) out[0] = acc;
 }
 
+
+// The same access pattern with the gathers issued as TMA bulk copies
+// (cp.async.bulk global -> shared, one per row, completion on an mbarrier), as
+// the step kernel's TMA paths do.  T: 10 plain, 11 hot evict_last / cold and
+// streams evict_first (cache_hint operand; 15: the same with the persisting
+// set-aside configured), 14 cold and streams evict_first only (16: with the
+// set-aside), 12 persisting window + plain
+// copies, 13 persisting window + evict_first on cold copies and streams.
+template <int T>
+__global__ void __launch_bounds__(256) gather_tma(const double2 *__restrict__ blk, int64_t rows,
+                                                  int64_t hot_rows, uint32_t p_hot32,
+                                                  int64_t n_gathers,
+                                                  const double2 *__restrict__ strm,
+                                                  int64_t strm_rows, double *out) {
+  __shared__ alignas(128) double2 buf[8][8][32];
+  __shared__ alignas(8) uint64_t bars[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[w]);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncwarp();
+  uint64_t pl, pf;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+  double acc = 0.0;
+  uint32_t phase = 0;
+  const int64_t per = 8;
+  constexpr bool SF = (T == 11 || T == 13 || T == 14 || T == 15 || T == 16);
+  for (int64_t g0 = warp * per; g0 < n_gathers; g0 += nwarps * per) {
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(4096)
+                   : "memory");
+    __syncwarp();
+    if (lane < per) {
+      const uint64_t h = mix((uint64_t)(g0 + lane));
+      const bool hot = (uint32_t)h < p_hot32;
+      const int64_t row = hot ? (int64_t)((h >> 32) % (uint64_t)hot_rows)
+                              : (int64_t)((h >> 32) % (uint64_t)rows);
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&buf[w][lane][0]);
+      const double2 *src = blk + row * 32;
+      const bool hinted = (T == 11 || T == 15) || ((T == 13 || T == 14 || T == 16) && !hot);
+      if (hinted) {
+        const uint64_t pol = ((T == 11 || T == 15) && hot) ? pl : pf;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1], %2, [%3], %4;" ::"r"(dst), "l"(src), "r"(512), "r"(bar), "l"(pol)
+            : "memory");
+      } else {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(dst), "l"(src), "r"(512), "r"(bar) : "memory");
+      }
+    }
+    const int64_t srow = (g0 / per) % strm_rows;
+    double2 s;
+    const double2 *sp = strm + srow * 32 + lane;
+    if (SF)
+      asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                   : "=d"(s.x), "=d"(s.y) : "l"(sp), "l"(pf));
+    else
+      s = __ldg(sp);
+    acc += s.x + s.y;
+    double2 *wp = const_cast<double2 *>(strm) + (strm_rows + srow) * 32 + lane;
+    if (SF)
+      asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(wp), "d"(s.x),
+                   "d"(s.y), "l"(pf) : "memory");
+    else
+      *wp = s;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(bar), "r"(phase) : "memory");
+    phase ^= 1;
+#pragma unroll
+    for (int q = 0; q < per; ++q) {
+      const double2 v = buf[w][q][lane];
+      acc += v.x * v.y;
+    }
+    __syncwarp();
+  }
+  if (acc == 123.456) out[0] = acc;
+}
+
+template <int T>
+static float run_tma(const double2 *blk, int64_t rows, int64_t hot_rows, double p_hot, int64_t ng,
+                     const double2 *strm, int64_t srows, double *out, int sms) {
+  const uint32_t p32 = (uint32_t)(p_hot * 4294967296.0);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  gather_tma<T><<<sms * 6, 256>>>(blk, rows, hot_rows, p32, ng / 4, strm, srows, out);  // warm
+  cudaEventRecord(a);
+  gather_tma<T><<<sms * 6, 256>>>(blk, rows, hot_rows, p32, ng, strm, srows, out);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
 template <int V>
 static float run(const double2 *blk, int64_t rows, int64_t hot_rows, double p_hot, int64_t ng,
                  const double2 *strm, int64_t srows, double *out, int sms) {
@@ -134,11 +238,13 @@ int main(int argc, char **argv) {
   cudaMemset(strm, 0, 2 * srows * row_bytes);
   const int64_t ng = 400ll << 20;  // gathers per timed launch (~200 GB)
   const double bytes = (double)ng * row_bytes * (1.0 + 2.0 / 8);
-  for (int v = 0; v <= 7; ++v) {
-    if (v == 5) continue;
+  for (int v = 0; v <= 16; ++v) {
+    if (v == 5 || v == 8 || v == 9) continue;
     if (only >= 0 && v != only) continue;
     cudaStreamAttrValue attr = {};
-    if (v == 2 || v == 3) {
+    if (v == 15 || v == 16)  // set-aside only, no window
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prop.persistingL2CacheMaxSize);
+    if (v == 2 || v == 3 || v == 12 || v == 13) {
       size_t setaside = prop.persistingL2CacheMaxSize;
       cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
       attr.accessPolicyWindow.base_ptr = blk;
@@ -159,13 +265,21 @@ int main(int argc, char **argv) {
       case 4: ms = run<4>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
       case 6: ms = run<6>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
       case 7: ms = run<7>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 10: ms = run_tma<10>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 11: ms = run_tma<11>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 12: ms = run_tma<12>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 13: ms = run_tma<13>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 14: ms = run_tma<14>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 15: ms = run_tma<15>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
+      case 16: ms = run_tma<16>(blk, rows, hot_rows, p_hot, ng, strm, srows, out, prop.multiProcessorCount); break;
     }
-    if (v == 2 || v == 3) {
+    if (v == 2 || v == 3 || v == 12 || v == 13) {
       attr.accessPolicyWindow.num_bytes = 0;
       cudaStreamSetAttribute(0, cudaStreamAttributeAccessPolicyWindow, &attr);
       cudaCtxResetPersistingL2Cache();
       cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
     }
+    if (v == 15 || v == 16) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
     cudaError_t e = cudaGetLastError();
     printf("variant %d hot %.0f MB p_hot %.2f: %.2f ms, %.0f GB/s requested, ideal DRAM share %.2f %s\n",
            v, hot_mb, p_hot, ms, bytes / ms / 1e6, 1.0 - p_hot * 8.0 / 10.0,
