@@ -118,6 +118,14 @@ int kpm_graph_from_csr32(kpm_ctx *ctx, int64_t n, const int64_t *indptr,
                          double shift, double scale, kpm_graph **out);
 
 int kpm_graph_info(kpm_graph *g, int64_t *n, int64_t *nnz, int64_t *max_degree);
+/* Build, ahead of the first run, whatever a run of k probe columns on this
+ * graph needs beside its own buffers -- for large implicit graphs the
+ * gather-ordered twin of the CSR (vertices renumbered by degree, each row's
+ * neighbours hottest-first; see kpm_run_create) -- so that a caller sizing
+ * probe batches from free memory sees it.  *twin = 1 when such runs step on
+ * the twin (their row sums then follow the twin's neighbour order, not the
+ * reference's; KPM_REORDER=0 disables, =1 forces). */
+int kpm_graph_prepare(kpm_graph *g, int64_t k, int32_t *twin);
 /* Copy the device CSR back (any pointer may be NULL): bit-exactness checks. */
 int kpm_graph_export(kpm_graph *g, int64_t *row_ptr, int32_t *col_idx,
                      double *dinv);

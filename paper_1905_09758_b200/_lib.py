@@ -63,6 +63,7 @@ SIGNATURES = {
                                     _c_dbl, _PP]),
     "kpm_graph_from_csr32": (_c_int, [_c_vp, _c_i64, _c_vp, _c_vp, _c_i64, _c_vp, _c_dbl,
                                       _c_dbl, _PP]),
+    "kpm_graph_prepare": (_c_int, [_c_vp, _c_i64, ctypes.POINTER(ctypes.c_int32)]),
     "kpm_graph_info": (_c_int, [_c_vp, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64),
                                 ctypes.POINTER(_c_i64)]),
     "kpm_graph_export": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp]),

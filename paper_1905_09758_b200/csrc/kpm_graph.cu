@@ -480,6 +480,91 @@ static int keys_to_graph(kpm_ctx *ctx, int64_t n, int s, uint64_t *keys,
   return KPM_OK;
 }
 
+// ---- gather-ordered twin (degree-descending renumbering) -----------------
+__global__ void relab_deg_keys(const int64_t *__restrict__ row_ptr, int64_t n,
+                               uint32_t *__restrict__ deg, int32_t *__restrict__ row) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    deg[i] = (uint32_t)(row_ptr[i + 1] - row_ptr[i]);
+    row[i] = (int32_t)i;
+  }
+}
+
+__global__ void relab_invert(const int32_t *__restrict__ perm, int64_t n,
+                             int32_t *__restrict__ iperm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    iperm[perm[i]] = (int32_t)i;
+}
+
+// one warp per (old) row: key = new_row << s | new_col
+__global__ void relab_keys(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           const int32_t *__restrict__ iperm, int64_t n, int s,
+                           uint64_t *__restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t o = warp; o < n; o += nwarps) {
+    const int64_t e0 = row_ptr[o], e1 = row_ptr[o + 1];
+    if (e1 == e0) continue;
+    const uint64_t hi = (uint64_t)(uint32_t)iperm[o] << s;
+    for (int64_t e = e0 + lane; e < e1; e += 32) keys[e] = hi | (uint64_t)(uint32_t)iperm[col[e]];
+  }
+}
+
+// The twin of an implicit, unpartitioned graph (see kpm_graph::relab); NULL
+// when it cannot be built (explicit values, partitions, out of memory).
+kpm_graph *graph_relabelled(kpm_graph *g) {
+  if (g->relab_state != 0) return g->relab;
+  g->relab_state = -1;
+  if (g->values || g->dinv_all || g->row0 != 0 || g->n_global != g->n || g->n < 2 || g->nnz < 1)
+    return nullptr;
+  cudaStream_t st = g->ctx->stream;
+  const int64_t n = g->n, nnz = g->nnz;
+  uint32_t *deg = nullptr, *deg2 = nullptr;
+  int32_t *row = nullptr, *perm = nullptr, *iperm = nullptr;
+  uint64_t *keys = nullptr, *alt = nullptr;
+  void *tmp = nullptr;
+  auto fail = [&]() -> kpm_graph * {
+    cudaGetLastError();
+    cudaFree(deg); cudaFree(deg2); cudaFree(row); cudaFree(perm); cudaFree(iperm);
+    cudaFree(keys); cudaFree(alt); cudaFree(tmp);
+    return nullptr;
+  };
+  if (cudaMalloc(&deg, 4 * n) || cudaMalloc(&deg2, 4 * n) || cudaMalloc(&row, 4 * n) ||
+      cudaMalloc(&perm, 4 * n) || cudaMalloc(&iperm, 4 * n))
+    return fail();
+  relab_deg_keys<<<grid_for(n), 256, 0, st>>>(g->row_ptr, n, deg, row);
+  size_t tb = 0;
+  // stable: equal degrees keep ascending row ids
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, deg, deg2, row, perm, (int)n, 0, 32, st);
+  if (cudaMalloc(&tmp, tb)) return fail();
+  cub::DeviceRadixSort::SortPairsDescending(tmp, tb, deg, deg2, row, perm, (int)n, 0, 32, st);
+  relab_invert<<<grid_for(n), 256, 0, st>>>(perm, n, iperm);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return fail();
+  cudaFree(tmp); tmp = nullptr;
+  cudaFree(deg); deg = nullptr;
+  cudaFree(deg2); deg2 = nullptr;
+  cudaFree(row); row = nullptr;
+  if (cudaMalloc(&keys, 8 * nnz) || cudaMalloc(&alt, 8 * nnz)) return fail();
+  const int s = key_bits(n);
+  relab_keys<<<grid_for(n * 32), 256, 0, st>>>(g->row_ptr, g->col_idx, iperm, n, s, keys);
+  if (cudaGetLastError() != cudaSuccess) return fail();
+  kpm_graph *t = nullptr;
+  const int rc = keys_to_graph(g->ctx, n, s, keys, alt, nnz, &t);  // frees keys / alt
+  keys = alt = nullptr;
+  if (rc != KPM_OK || !t || t->nnz != nnz) {
+    if (t) kpm_graph_free(t);
+    return fail();
+  }
+  t->perm = perm;
+  t->iperm = iperm;
+  t->relab_state = -1;  // a twin has no twin
+  g->relab = t;
+  g->relab_state = 1;
+  return t;
+}
+
 __global__ void idx64_to_32(const int64_t *__restrict__ in, int64_t m,
                             int64_t n, int32_t *__restrict__ out, int *bad) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
@@ -796,6 +881,9 @@ void kpm_graph_free(kpm_graph *g) {
   cudaFree(g->heavy_rows);
   cudaFree(g->chunk_order);
   cudaFree(g->dinv_all);
+  cudaFree(g->perm);
+  cudaFree(g->iperm);
+  if (g->relab) kpm_graph_free(g->relab);
   delete g;
 }
 

@@ -120,7 +120,19 @@ struct kpm_graph {
   // rows per degree bucket, 8 buckets per octave (bucket b holds degrees
   // [deg_bucket_lo(b), deg_bucket_lo(b + 1)); finish_graph): hot-row L2 policy
   unsigned long long deg_hist[kDegBuckets] = {};
+  // gather-ordered twin (kpm_graph_relabelled): the same graph with vertices
+  // renumbered by degree descending (ties by id) and every row's neighbour list
+  // sorted by the new ids, i.e. hottest neighbours first; built on demand for
+  // large implicit graphs, owned by this graph.  In the twin, perm[new] = old
+  // and iperm[old] = new.
+  kpm_graph *relab = nullptr;
+  int relab_state = 0;  // 0 not tried, 1 built, -1 unavailable
+  int32_t *perm = nullptr, *iperm = nullptr;
 };
+
+namespace kpm {
+kpm_graph *graph_relabelled(kpm_graph *g);  // kpm_graph.cu; NULL when unavailable
+}
 
 #define KPM_MAX_PARTS 16
 
@@ -128,7 +140,9 @@ struct kpm_graph {
 static constexpr int64_t kHeavyDegree = 65536;
 
 struct kpm_run {
-  kpm_graph *g = nullptr;
+  kpm_graph *g = nullptr;       // the graph the step kernels walk (user_g or its twin)
+  kpm_graph *user_g = nullptr;  // the graph the caller passed
+  double *unperm = nullptr;     // kpm_run_block scratch: T_k in the caller's row order
   int64_t k = 0;      // probes in this batch
   int64_t ld = 0;     // padded row stride (doubles)
   int cpl = 1;        // columns per lane (1, 2, 4)

@@ -84,9 +84,16 @@ struct StepParams {
   int fuse_tiles;          // run all 64-column tiles of a step as one launch
   int g4hot;               // hot-ordered gather4 waves with L2 policies (light_g4 HOT)
   double hot_dinv_g4;      // hot rows of the gather4 path: dinv_j <= hot_dinv_g4
+  int hot_rows;            // gather-ordered twin: gathered ids < hot_rows are hot (L2 policy)
+  const int32_t *perm;     // gather-ordered twin: perm[row] = the caller's row id (else NULL)
   int64_t hub_off;         // dynamic smem (doubles) of warp 0's hub ring (kpm_step_kernel)
   unsigned long long *trace;  // KPM_TRACE: per work item (start ns, end ns, smid<<32|warp)
 };
+
+// row id in the caller's numbering (per-node outputs of a run on the twin)
+__device__ __forceinline__ size_t out_row(const StepParams &p, int64_t row) {
+  return p.perm ? (size_t)p.perm[row] : (size_t)row;
+}
 
 // KPM_TRACE diagnostics: one record per work item of one traced launch
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -468,9 +475,9 @@ __device__ __forceinline__ void light_chunk(const StepParams &p, int chunk, doub
         if constexpr (INIT) {
           // kpm.py:144-147: den = einsum(z, z) (same reduction as num[0])
           double *den = const_cast<double *>(p.den);
-          den[i] = num;  // zero mass is checked on the final den (kpm_run_result)
+          den[out_row(p, i)] = num;  // zero mass is checked on the final den (kpm_run_result)
         }
-        p.ldos[(size_t)i * p.ldos_stride + p.ldos_col] = num;  // raw num[m, i]
+        p.ldos[out_row(p, i) * p.ldos_stride + p.ldos_col] = num;  // raw num[m, i]
       }
     }
   }
@@ -532,7 +539,7 @@ __device__ __forceinline__ void stream_finish_row(const StepParams &p, int row, 
     const double num = warp_sum_fixed(lsum);
     if (lane == 0) {
       if (!isfinite(num)) atomicOr(p.flag, 1);
-      p.ldos[(size_t)row * p.ldos_stride + p.ldos_col] = num;
+      p.ldos[out_row(p, row) * p.ldos_stride + p.ldos_col] = num;
     }
   }
 }
@@ -797,7 +804,7 @@ __device__ __forceinline__ void bulk_finish_row(const StepParams &p, int row, bo
     const double num = warp_sum_fixed(lsum);
     if (lane == 0) {
       if (!isfinite(num)) atomicOr(p.flag, 1);
-      p.ldos[(size_t)row * p.ldos_stride + p.ldos_col] = num;
+      p.ldos[out_row(p, row) * p.ldos_stride + p.ldos_col] = num;
     }
   }
 }
@@ -1484,8 +1491,14 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
   // T_{k+1}, the cold gathers) carries L2 evict_first, so that the hot rows --
   // gathered with NO hint -- stay resident (tools/exp/l2policy.cu: evict_last
   // on TMA copies does not hold lines, evict_first on the cold traffic does)
-  uint64_t pol_first = 0;
-  if constexpr (HOT) pol_first = l2_policy_first();
+  // the same stream policy applies on the gather-ordered twin (hot_rows > 0),
+  // where a gather4 group is cold when its four ids are all >= hot_rows; one
+  // code path: the stream operands always carry a policy, evict_first when a
+  // hot set is protected, evict_normal otherwise
+  constexpr bool SH = true;
+  uint64_t pol_first;
+  if (HOT || p.hot_rows > 0) pol_first = l2_policy_first();
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_first));
   const uint32_t rows_sa = smem_u32(base);
   const uint32_t wv_sa = rows_sa + L::rows_d * 8;
   const uint32_t col_sa = wv_sa + L::wv_d * 8;
@@ -1516,7 +1529,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       const size_t off = (size_t)r * ld + c0;
       const uint32_t dst = own_sa + (uint32_t)(sl * NOP * W + lane * C) * 8;
       int q = 0;
-      if constexpr (HOT) {
+      if constexpr (SH) {
         // the own row of T_k is also gathered by its neighbours: no hint
         if constexpr (EXPL || MODE == MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.X + off);
         if constexpr (!FIRST) cp_async_cols_hint<C>(dst + (q++) * W * 8, p.Xprev + off, pol_first);
@@ -1547,7 +1560,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
   auto issue_col = [&](int w) {
     const int e = w * WAVE + lane;
     if (lane < WAVE && e < nnz) {
-      if constexpr (HOT) cp_async_4_first(col_slot(w) + lane * 4, p.col + K0 + e, pol_first);
+      if constexpr (SH) cp_async_4_first(col_slot(w) + lane * 4, p.col + K0 + e, pol_first);
       else cp_async_4(col_slot(w) + lane * 4, p.col + K0 + e);
     }
   };
@@ -1606,10 +1619,20 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
                         j[4 * q + 2], j[4 * q + 3], bar);
         }
       } else {
+        // gather-ordered twin: rows are sorted hottest-first, so whole groups
+        // are cold (all four ids >= hot_rows) without any reordering
 #pragma unroll
-        for (int q = 0; q < WAVE / 4; ++q)
-          tma_gather4(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1], j[4 * q + 2],
-                      j[4 * q + 3], bar);
+        for (int q = 0; q < WAVE / 4; ++q) {
+          const bool cold = p.hot_rows > 0 && j[4 * q] >= p.hot_rows &&
+                            j[4 * q + 1] >= p.hot_rows && j[4 * q + 2] >= p.hot_rows &&
+                            j[4 * q + 3] >= p.hot_rows;
+          if (cold)
+            tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
+                             j[4 * q + 2], j[4 * q + 3], bar, pol_first);
+          else
+            tma_gather4(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
+                        j[4 * q + 2], j[4 * q + 3], bar);
+        }
       }
     }
     if (!HOT && lane < cnt) {
@@ -1685,8 +1708,8 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       if constexpr (!FIRST) lds_cols<C>(a + (q++) * W * 8, pv);
       if constexpr (MODE != MODE_DBL) lds_cols<C>(a + (q++) * W * 8, zv);
     }
-    bulk_finish_row<C, MODE, EXPL, FIRST, HOT>(p, r, active, c0, acc, xo, pv, zv, s1, s2,
-                                               pol_first);
+    bulk_finish_row<C, MODE, EXPL, FIRST, SH>(p, r, active, c0, acc, xo, pv, zv, s1, s2,
+                                              pol_first);
     issue_own(r + R);
   };
   auto advance = [&](int64_t kk) {
@@ -1960,13 +1983,13 @@ __global__ void finalize_kernel(const double *__restrict__ gpart, int n_groups,
 // LDOS hub rows: sum the per-slice partials in slice order.
 __global__ void ldos_heavy_kernel(const double *__restrict__ hldos, const int32_t *rows,
                                   int n_heavy, int nsl, double *ldos, int64_t stride,
-                                  int col, int32_t *flag) {
+                                  int col, int32_t *flag, const int32_t *perm) {
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
   if (h >= n_heavy) return;
   double s = hldos[(size_t)h * nsl];
   for (int q = 1; q < nsl; ++q) s = __dadd_rn(s, hldos[(size_t)h * nsl + q]);
   if (!isfinite(s)) atomicOr(flag, 1);
-  ldos[(size_t)rows[h] * stride + col] = s;
+  ldos[(size_t)(perm ? perm[rows[h]] : rows[h]) * stride + col] = s;
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -2255,6 +2278,15 @@ static StepParams base_params(const kpm_run *r) {
   }
   // hot rows of the gather4 path (hot-ordered waves): same rule over the
   // gathered segment (64-column tiles for the 4-column layouts)
+  // gather-ordered twin: the hottest rows (lowest new ids) stay unhinted, every
+  // other gather is evict_first (profiles/r02_ncu_summary.md: flat between 100k and 400k rows)
+  p.perm = g->perm;
+  p.hot_rows = 0;
+  if (g->perm) {
+    p.hot_rows = 250000;
+    if (const char *e = getenv("KPM_HOT_ROWS")) p.hot_rows = atoi(e);
+    if (p.hot_rows > g->n) p.hot_rows = (int)g->n;
+  }
   p.hot_dinv_g4 = -1.0;
   {
     double hot_bytes = 64.0 * 1024 * 1024;
@@ -2268,6 +2300,7 @@ static StepParams base_params(const kpm_run *r) {
     // for the 1-column layout (C3/C5 P=32: +4%)
     p.g4hot = tiled && 8.0 * (double)seg * (double)g->n > 200.0 * (double)g->ctx->l2_bytes;
     if (const char *e = getenv("KPM_G4_HOT")) p.g4hot = atoi(e);
+    if (g->perm) p.g4hot = 0;  // the twin's rows are already hot-first
     const double budget = hot_bytes / (8.0 * (double)seg);
     double rows = 0.0, hot_deg = 0.0;
     for (int b = kDegBuckets - 1; b >= 0; --b) {
@@ -2322,7 +2355,7 @@ __device__ __forceinline__ void philox4x64_10(uint64_t c[4], uint64_t k0, uint64
 // Rows [row0, row0+n) of the columns (global row i -> local row i - row0).
 __global__ void rademacher_kernel(int64_t n, int64_t ncols, const uint64_t *__restrict__ keys,
                                   double *__restrict__ z, int64_t ldz, int64_t col0,
-                                  int64_t row0) {
+                                  int64_t row0, const int32_t *__restrict__ iperm = nullptr) {
   const int64_t b0 = row0 / 8, nblk = (row0 + n + 7) / 8 - b0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nblk * ncols;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -2334,9 +2367,24 @@ __global__ void rademacher_kernel(int64_t n, int64_t ncols, const uint64_t *__re
       const int64_t i = b * 8 + q - row0;
       if (i >= 0 && i < n) {
         const uint32_t half = (q & 1) ? (uint32_t)(c[q >> 1] >> 32) : (uint32_t)c[q >> 1];
-        z[i * ldz + col0 + j] = (half >> 31) ? -1.0 : 1.0;
+        const int64_t io = iperm ? (int64_t)iperm[i] : i;  // row of a run on the twin
+        z[io * ldz + col0 + j] = (half >> 31) ? -1.0 : 1.0;
       }
     }
+  }
+}
+
+// rows of a block between the caller's order and the twin's: out[r] = in[perm[r]]
+// (gather) or out[perm[r]] = in[r] (scatter), ld doubles per row
+__global__ void permute_rows_kernel(const double *__restrict__ in, double *__restrict__ out,
+                                    const int32_t *__restrict__ perm, int64_t n, int64_t ld,
+                                    int scatter) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * ld;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / ld, c = t - r * ld;
+    const int64_t o = perm[r];
+    if (scatter) out[o * ld + c] = in[t];
+    else out[t] = in[o * ld + c];
   }
 }
 
@@ -2493,6 +2541,35 @@ static void encode_block_maps(kpm_run *r) {
 
 extern "C" {
 
+// Large implicit graphs step on the gather-ordered twin (kpm_graph::relab):
+// rows renumbered by degree, each row's neighbours hottest-first, so the
+// popular rows of T_k stay in L2 (evict_first on everything else).  A row's
+// sum then adds its neighbours in that order instead of ascending original
+// id -- deterministic and independent of the probe count, but not the
+// reference's rounding sequence; KPM_REORDER=0 keeps the reference's order
+// (bit-identical T_k), KPM_REORDER=1 forces the twin.  Default: when one
+// gathered column tile of T_k is >= 32x the L2.
+static kpm_graph *stepping_graph(kpm_graph *g, int64_t k) {
+  int want = -1;
+  if (const char *e = getenv("KPM_REORDER")) want = atoi(e);
+  const int cpl = k <= 32 ? 1 : (k <= 64 ? 2 : 4);
+  const int64_t ld = (k + cpl - 1) / cpl * cpl;
+  const double seg = (double)(cpl == 4 ? (ld < kTileW ? ld : kTileW) : ld);
+  const bool big = 8.0 * seg * (double)g->n >= 32.0 * (double)g->ctx->l2_bytes;
+  if (want == 1 || (want < 0 && big)) {
+    if (kpm_graph *t = kpm::graph_relabelled(g)) return t;
+  }
+  return g;
+}
+
+int kpm_graph_prepare(kpm_graph *g, int64_t k, int32_t *twin) {
+  KPM_CHECK_ARG(g && k >= 1, "bad arguments");
+  KPM_CUDA(cudaSetDevice(g->ctx->device));
+  kpm_graph *s = stepping_graph(g, k);
+  if (twin) *twin = s != g ? 1 : 0;
+  return KPM_OK;
+}
+
 int kpm_run_create(kpm_graph *g, int64_t k, int32_t mode, int32_t m_max,
                    int32_t flags, kpm_run **out) {
   KPM_CHECK_ARG(g && out, "bad arguments");
@@ -2505,10 +2582,12 @@ int kpm_run_create(kpm_graph *g, int64_t k, int32_t mode, int32_t m_max,
                 "partition graph needs kpm_graph_set_dinv first");
   KPM_CUDA(cudaSetDevice(g->ctx->device));
   kpm_run *r = new kpm_run();
-  r->g = g;
+  r->user_g = g;
   r->k = k;
   r->cpl = k <= 32 ? 1 : (k <= 64 ? 2 : 4);
   r->ld = (k + r->cpl - 1) / r->cpl * r->cpl;
+  g = stepping_graph(g, k);
+  r->g = g;
   r->mode = mode;
   r->m_max = m_max;
   r->flags = flags;
@@ -2577,9 +2656,23 @@ int kpm_run_set_probes(kpm_run *r, const double *z, int64_t ldz) {
   KPM_CHECK_ARG(ldz >= r->k, "ldz < k");
   KPM_CUDA(cudaSetDevice(r->g->ctx->device));
   cudaStream_t st = r->g->ctx->stream;
-  if (r->g->n > 0)
+  if (r->g->n > 0 && r->g->perm) {
+    // the caller's rows -> the twin's order, staged through T_1's block
+    double *tmp = r->b;
+    if (!tmp) KPM_CUDA(cudaMalloc(&tmp, sizeof(double) * (size_t)r->g->n * r->ld));
+    KPM_CUDA(cudaMemcpy2DAsync(tmp, sizeof(double) * r->ld, z, sizeof(double) * ldz,
+                               sizeof(double) * r->k, r->g->n, cudaMemcpyDefault, st));
+    permute_rows_kernel<<<grid_of(r->g->n * r->ld), 256, 0, st>>>(tmp, r->a, r->g->perm, r->g->n,
+                                                                 r->ld, 0);
+    KPM_CUDA(cudaGetLastError());
+    if (!r->b) {
+      KPM_CUDA(cudaStreamSynchronize(st));
+      cudaFree(tmp);
+    }
+  } else if (r->g->n > 0) {
     KPM_CUDA(cudaMemcpy2DAsync(r->a, sizeof(double) * r->ld, z, sizeof(double) * ldz,
                                sizeof(double) * r->k, r->g->n, cudaMemcpyDefault, st));
+  }
   return run_after_probes(r);
 }
 
@@ -2594,7 +2687,7 @@ int kpm_run_set_rademacher(kpm_run *r, const uint64_t *keys) {
   const int64_t n = r->g->n;
   if (n > 0)
     rademacher_kernel<<<grid_of(((n + 15) / 8) * r->k), 256, 0, st>>>(
-        n, r->k, (const uint64_t *)dk, r->a, r->ld, 0, r->g->row0);
+        n, r->k, (const uint64_t *)dk, r->a, r->ld, 0, r->g->row0, r->g->iperm);
   KPM_CUDA(cudaGetLastError());
   int rc = run_after_probes(r);
   return rc;
@@ -2723,7 +2816,8 @@ int kpm_run_advance(kpm_run *r, int32_t steps, int32_t *remaining) {
     if (r->mode == KPM_MODE_LDOS && r->g->n_heavy > 0) {
       const int nsl = (int)((r->ld + kSlice - 1) / kSlice);
       ldos_heavy_kernel<<<(r->g->n_heavy + 127) / 128, 128, 0, st>>>(
-          r->hldos, r->g->heavy_rows, r->g->n_heavy, nsl, r->ldos, r->m_max + 1, m, r->flag);
+          r->hldos, r->g->heavy_rows, r->g->n_heavy, nsl, r->ldos, r->m_max + 1, m, r->flag,
+          r->g->perm);
       KPM_CUDA(cudaGetLastError());
     }
     if (r->mode == KPM_MODE_DOS_DOUBLING) KPM_CUDA(launch_finalize(r, 2, m, st));
@@ -2850,6 +2944,17 @@ int kpm_run_trim(kpm_run *r) {
 int kpm_run_block(kpm_run *r, const double **t_k, int64_t *ld, int32_t *k_index) {
   KPM_CHECK_ARG(r, "run is NULL");
   if (t_k) *t_k = r->cur;
+  if (t_k && r->g->perm && r->cur && r->g->n > 0) {
+    // a run on the twin: hand out T_k in the caller's row order
+    KPM_CUDA(cudaSetDevice(r->g->ctx->device));
+    cudaStream_t st = r->g->ctx->stream;
+    if (!r->unperm) KPM_CUDA(cudaMalloc(&r->unperm, sizeof(double) * (size_t)r->g->n * r->ld));
+    permute_rows_kernel<<<grid_of(r->g->n * r->ld), 256, 0, st>>>(r->cur, r->unperm, r->g->perm,
+                                                                 r->g->n, r->ld, 1);
+    KPM_CUDA(cudaGetLastError());
+    KPM_CUDA(cudaStreamSynchronize(st));
+    *t_k = r->unperm;
+  }
   if (ld) *ld = r->ld;
   if (k_index) *k_index = r->k_index;
   return KPM_OK;
@@ -2871,6 +2976,7 @@ void kpm_run_free(kpm_run *r) {
   cudaFree(r->hldos);
   cudaFree(r->gpart);
   cudaFree(r->queue);
+  cudaFree(r->unperm);
   for (cudaEvent_t e : r->ev) cudaEventDestroy(e);
   delete r;
 }

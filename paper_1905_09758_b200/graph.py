@@ -243,6 +243,16 @@ class DeviceGraph:
             ctypes.byref(h)), "graph_rmat")
         return cls(h.value, ctx)
 
+    def prepare(self, k) -> bool:
+        """Build what runs of k probe columns need beside their own buffers
+        (the gather-ordered twin of a large implicit graph, kpm_graph_prepare)
+        before batch sizes are derived from free memory.  True when such runs
+        step on the twin."""
+        twin = ctypes.c_int32(0)
+        _lib.check(_lib.load().kpm_graph_prepare(self.handle, int(k), ctypes.byref(twin)),
+                   "graph_prepare")
+        return bool(twin.value)
+
     def on(self, ctx) -> "DeviceGraph":
         """This graph on context `ctx`: itself, or a cached replica copied
         device to device (peer copy over NVLink for another GPU)."""

@@ -162,6 +162,7 @@ def _batch_cols(dev, nz, blocks, max_cols=1024, fixed_bytes=0):
     """Probe columns per batch: all of them when two/three n x ld fp64 blocks
     (plus `fixed_bytes` of per-run buffers, e.g. the (n, M+1) LDOS result)
     fit in 85% of free HBM, else the largest multiple of 32 that does."""
+    dev.prepare(min(nz, max_cols, 128))  # the twin (if any) exists before free memory is read
     free, _ = dev.ctx.mem_info()
     per_col = 8 * max(dev.n, 1) * blocks
     fit = int(max(0.85 * free - fixed_bytes, 0) // per_col)

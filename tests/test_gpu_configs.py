@@ -94,13 +94,19 @@ def _subset_vs_fixture(cfg, scale, seed, family):
     dev.free()
 
 
-def test_c3_probe_subset_full_length_vs_reference(kpm_ctx):
-    """C3: columns 0-3 of the 128-probe family x all 500 moments."""
+@pytest.mark.parametrize("order", ["reference", "twin"])
+def test_c3_probe_subset_full_length_vs_reference(kpm_ctx, monkeypatch, order):
+    """C3: columns 0-3 of the 128-probe family x all 500 moments -- in the
+    reference's neighbour order (what 4 columns run by default) and on the
+    gather-ordered twin (what the 128-probe batches of the bench run)."""
+    monkeypatch.setenv("KPM_REORDER", "1" if order == "twin" else "0")
     _subset_vs_fixture("c3", 24, 2, 128)
 
 
-def test_c5_probe_subset_full_length_vs_reference(kpm_ctx):
+@pytest.mark.parametrize("order", ["reference", "twin"])
+def test_c5_probe_subset_full_length_vs_reference(kpm_ctx, monkeypatch, order):
     """C5: columns 0-1 of the 256-probe family x the first 100 moments."""
+    monkeypatch.setenv("KPM_REORDER", "1" if order == "twin" else "0")
     _subset_vs_fixture("c5", 26, 4, 256)
 
 

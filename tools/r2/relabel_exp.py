@@ -45,7 +45,17 @@ def relabel(dev):
         b = min(nnz, a + step)
         pos = torch.arange(a, b, device=cuda, dtype=torch.int64) + offs[rows_of[a:b]]
         ci2[a:b] = inv[ci[pos].long()].int()
-    del rows_of, ci, rp, offs, inv, order
+    del ci, rp, offs, inv, order
+    if os.environ.get("KPM_EXP_SORT", "1") == "1":
+        # canonical CSR of the relabelled graph: each row sorted by new id,
+        # i.e. by degree descending -- the hot neighbours first
+        key = rows_of * n + ci2.long()
+        del rows_of
+        key = torch.sort(key)[0]
+        ci2 = (key % n).int()
+        del key
+    else:
+        del rows_of
     torch.cuda.synchronize()
     g2 = kp.DeviceGraph.from_csr(n, rp2.data_ptr(), (ci2.data_ptr(), nnz, "int32"), ctx=dev.ctx)
     del rp2, ci2
@@ -71,6 +81,7 @@ def main():
     ap.add_argument("--scale", type=int, default=26)
     ap.add_argument("--only", default="")
     ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--hotk", type=int, nargs="+", default=[0])
     a = ap.parse_args()
     ctx = _lib.Context.get(0)
     dev = kp.DeviceGraph.rmat(a.scale, 16, 4, ctx=ctx)
@@ -82,11 +93,13 @@ def main():
         if a.only and name != a.only:
             continue
         for P in a.probes:
-            ms = time_steps(g, P, a.steps)
-            print(json.dumps({"graph": name, "P": P, "ms_per_step": round(ms, 2),
-                              "window_mb": os.environ.get("KPM_WINDOW_MB", "0"),
-                              "g4hot": os.environ.get("KPM_G4_HOT", "default"),
-                              "relabel_s": round(t_rel, 2)}), flush=True)
+            for hotk in (a.hotk if name == "relab" else [0]):
+                os.environ["KPM_EXP_HOTK"] = str(hotk)
+                ms = time_steps(g, P, a.steps)
+                print(json.dumps({"graph": name, "P": P, "hotk": hotk, "ms_per_step": round(ms, 2),
+                                  "window_mb": os.environ.get("KPM_WINDOW_MB", "0"),
+                                  "g4hot": os.environ.get("KPM_G4_HOT", "default"),
+                                  "relabel_s": round(t_rel, 2)}), flush=True)
 
 
 if __name__ == "__main__":
