@@ -166,7 +166,14 @@ int kpm_filter_probes(kpm_ctx *ctx, int64_t n, int64_t k, double *z,
 /* --------------------------------------------------------- recurrence --- */
 /* A moment run over one probe batch: dos_moments (kpm.py:92-117) or
  * pdos_moments (kpm.py:120-152).  The run owns two n x ld fp64 recurrence
- * blocks (three for DIRECT/LDOS: the probes stay resident). */
+ * blocks (three for DIRECT/LDOS: the probes stay resident).
+ * Neighbour order: a row's sum adds its neighbours in the CSR's stored order
+ * (_spmv.pyx:11-39), so T_k is bit-identical to the reference -- except for
+ * large implicit graphs (one gathered column tile of T_k >= 32x the L2), which
+ * step on the gather-ordered twin (kpm_graph_prepare): another fixed order,
+ * same tolerances on every result, rows of every input/output still in the
+ * caller's numbering.  Environment KPM_REORDER=0 always keeps the CSR's order,
+ * =1 forces the twin where one can be built. */
 int kpm_run_create(kpm_graph *g, int64_t k, int32_t mode, int32_t m_max,
                    int32_t flags, kpm_run **out);
 /* probes: n x k row-major with row stride ldz (host-or-device) */
@@ -204,7 +211,8 @@ int kpm_run_accumulate(kpm_run *dst, kpm_run *src);
 /* Free the recurrence blocks of a completed run, keeping its results (the
  * (m_max+1) x k contributions or the n x (m_max+1) LDOS sums). */
 int kpm_run_trim(kpm_run *r);
-/* Device pointer of the current T_k block and its row stride (tests). */
+/* Device pointer of the current T_k block and its row stride (tests); for a
+ * run on the twin a copy in the caller's row order (valid until the next call). */
 int kpm_run_block(kpm_run *r, const double **t_k, int64_t *ld, int32_t *k_index);
 void kpm_run_free(kpm_run *r);
 

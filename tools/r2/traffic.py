@@ -52,7 +52,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(REPO, "gpurun_out", "traffic.json"))
     a = ap.parse_args()
     rec = {"note": "DRAM bytes of one fused step launch, keyed config/P; valid while "
-                   "kernel_sha == bench.kernel_hash() (tests/test_host.py checks it)",
+                   "kernel_sha == bench.kernel_hash() (tests/test_bench_contract.py checks it)",
            "entries": {}}
     if os.path.exists(a.out):
         with open(a.out) as f:
