@@ -283,6 +283,7 @@ def run_ours(args):
     t_build = time.time() - t0
     n, nnz = dev.n, dev.nnz
 
+    twin = dev.prepare(min(P, args.batch))  # builds the gather-ordered twin when runs use it
     c0, c1 = shard_range(P, rank, world)
     emu = args.shard_of if (world == 1 and args.shard_of > 1) else 0
     if emu:  # one GPU runs rank 0's shard of an emu-way split (scaling projection)
@@ -372,8 +373,9 @@ def run_ours(args):
         "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4), "traffic": tr["dram_bytes"] if tr else None,
         "basis": basis, "peak_kind": peak_kind,
-        "kernel": "kpm_step_g4_kernel (TMA gather4; P>64 as fused 64-column tiles), "
-                  f"batch of {pw} columns",
+        "kernel": "kpm_step_g4_kernel (TMA gather4; P>64 as fused 64-column tiles"
+                  + ("; gather-ordered twin, evict_first on cold traffic" if twin else "")
+                  + f"), batch of {pw} columns",
         "kernel_ms": round(kern_avg, 3), "kernel_sha": kernel_hash(),
         "traffic_source": tr.get("source") if tr else None,
         "frac_model_upper_bound": round(model / kern_s / 1e9 / peak, 4),
@@ -413,6 +415,10 @@ def run_ours(args):
                                       "all-reduce of the (M+1) x P contributions per job",
                        "l2": "inputs larger than L2 (%.1f GB blocks per batch)"
                              % (8 * n * pw / 1e9),
+                       "neighbour_order": ("gather-ordered twin: degree-renumbered CSR, rows "
+                                           "hottest-first (default at this size; KPM_REORDER=0 "
+                                           "= the reference's order)" if twin
+                                           else "the reference's CSR order"),
                        "graph_build_s": round(t_build, 3), "probe_gen_s": round(t_probes, 4),
                        "allreduce_ms": round(ar_ms, 3),
                        "per_spmm_value": round(value / 2, 3),

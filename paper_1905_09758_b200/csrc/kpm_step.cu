@@ -82,8 +82,6 @@ struct StepParams {
   int lean;                // per-lane async gathers for C <= 2 (light_lean)
   int ntiles;              // gather4: light items per chunk = 64-column tiles of one launch
   int fuse_tiles;          // run all 64-column tiles of a step as one launch
-  int g4hot;               // hot-ordered gather4 waves with L2 policies (light_g4 HOT)
-  double hot_dinv_g4;      // hot rows of the gather4 path: dinv_j <= hot_dinv_g4
   int hot_rows;            // gather-ordered twin: gathered ids < hot_rows are hot (L2 policy)
   const int32_t *perm;     // gather-ordered twin: perm[row] = the caller's row id (else NULL)
   int64_t hub_off;         // dynamic smem (doubles) of warp 0's hub ring (kpm_step_kernel)
@@ -905,8 +903,11 @@ __device__ __forceinline__ void light_bulk(const StepParams &p, int chunk, BulkR
   int jc = ld_col(0), jn = ld_col(1), jnn = 0;
   double wc = ld_w(0, jc), wn = 0.0;
   int64_t cur_b = 0;  // batch held in (jc, wc)
-  const bool hints = p.hot_dinv > 0.0;
-  const uint64_t pol_last = hints ? l2_policy_last() : 0, pol_first = hints ? l2_policy_first() : 0;
+  // L2 policy (profiles/r02_ncu_summary.md section 3): cold rows evict_first, hot
+  // rows no hint (evict_last on TMA copies does not hold lines); hot = id below
+  // hot_rows on the gather-ordered twin, else a degree threshold
+  const bool hints = p.hot_dinv > 0.0 || p.hot_rows > 0;
+  const uint64_t pol_first = hints ? l2_policy_first() : 0;
   auto issue = [&](int64_t w) {  // wave w -> slots (w % nw) * kBulkWave + k
     const int64_t e0 = w * kBulkWave;
     if (e0 >= nnz) return;
@@ -935,11 +936,11 @@ __device__ __forceinline__ void light_bulk(const StepParams &p, int chunk, BulkR
         const int L = base + k;
         ring.wv[L] = wv;
         bool hot = false;
-        if constexpr (!EXPL) hot = wv <= p.hot_dinv;
+        if (p.hot_rows > 0) hot = j < p.hot_rows;
+        else if constexpr (!EXPL) hot = wv <= p.hot_dinv;
         bulk_gather(ring.slot + (size_t)L * ld,
                     p.nparts <= 1 ? p.X + (size_t)(uint32_t)j * (uint32_t)ld : gather_row(p, (uint32_t)j),
-                    rbytes, ring.bar + g,
-                    hints ? 1 : 0, hot ? pol_last : pol_first);
+                    rbytes, ring.bar + g, (hints && !hot) ? 1 : 0, pol_first);
       } else {
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(ring.bar + g))
                      : "memory");
@@ -1415,8 +1416,8 @@ struct G4 {
   static constexpr int W = 32 * C;
   static constexpr int slot_d = ((WAVE * W * 8 + 127) / 128) * 128 / 8;  // one wave's rows
   static constexpr int rows_d = D * slot_d;
-  static constexpr int wv_d = 2 * D * WAVE;   // [2D][WAVE] doubles (hot order: 2 slots at D=1)
-  static constexpr int col_d = 2 * D * WAVE;  // [4D][WAVE] int32 (default order uses 2D)
+  static constexpr int wv_d = 2 * D * WAVE;   // [D][WAVE] doubles used (sized for 2D)
+  static constexpr int col_d = 2 * D * WAVE;  // [2D][WAVE] int32 used (sized for 4D)
   static constexpr int own_d = R * (NOP > 0 ? NOP : 1) * W;
   static constexpr int bar_d = D + R;
   static constexpr int data_d = rows_d + wv_d + col_d + own_d;
@@ -1454,22 +1455,12 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm,
       : "memory");
 }
 
-// HOT (hot-ordered waves, D == 1, implicit values only): each wave's weights
-// dinv_j are fetched one wave ahead of its rows, so the issuing warp knows
-// which neighbours are hot (dinv_j <= hot_dinv_g4: the highest-degree rows
-// whose segments fill the hot budget of L2) before the gathers go out.  The
-// wave's rows land hot-first in shared memory (stable partition), so whole
-// gather4 groups carry one L2 policy: all-hot groups evict_last, all-cold
-// groups evict_first, a mixed group none.  The consumer still adds neighbour k
-// of the wave in CSR order, reading its row from position pos_k (one shuffle),
-// so sums and results are bitwise those of the default order.
-template <int C, int MODE, bool EXPL, bool FIRST, bool HOT>
+template <int C, int MODE, bool EXPL, bool FIRST>
 __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap *tm, int chunk,
                                          const int64_t col0, const int64_t tw, double *base,
                                          uint32_t &ophase, uint32_t &wphase) {
   using L = G4<C, MODE, EXPL, FIRST>;
   constexpr int D = L::D, R = L::R, W = L::W, NOP = L::NOP, WAVE = L::WAVE;
-  static_assert(!HOT || (D == 1 && !EXPL), "hot-ordered waves need D == 1 and dinv weights");
   const int lane = threadIdx.x & 31;
   const int64_t ld = p.ld;
   // this launch's column tile [col0, col0 + tw): lane l owns columns col0 + [lC, lC + C)
@@ -1487,17 +1478,18 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     }
     return;
   }
-  // HOT: everything that is read or written once per step (col ids, own rows,
-  // T_{k+1}, the cold gathers) carries L2 evict_first, so that the hot rows --
-  // gathered with NO hint -- stay resident (tools/exp/l2policy.cu: evict_last
-  // on TMA copies does not hold lines, evict_first on the cold traffic does)
-  // the same stream policy applies on the gather-ordered twin (hot_rows > 0),
-  // where a gather4 group is cold when its four ids are all >= hot_rows; one
-  // code path: the stream operands always carry a policy, evict_first when a
-  // hot set is protected, evict_normal otherwise
-  constexpr bool SH = true;
+  // L2 policy (tools/exp/l2policy.cu, profiles/r02_ncu_summary.md): on this
+  // part evict_last does not hold TMA-copied lines, the stream access-policy
+  // window does not apply to TMA reads, but evict_first on everything that is
+  // touched once per step does protect the rest.  On the gather-ordered twin
+  // (hot_rows > 0: ids are degree ranks, rows list their hottest neighbours
+  // first) a gather4 group whose four ids are all >= hot_rows is cold: cold
+  // groups, the own rows of T_{k-1} / z, the col ids and the T_{k+1} stores
+  // carry evict_first, groups with a hot row no hint.  One code path: the
+  // stream operands always carry a policy, evict_normal when nothing is
+  // protected (the caller's CSR order).
   uint64_t pol_first;
-  if (HOT || p.hot_rows > 0) pol_first = l2_policy_first();
+  if (p.hot_rows > 0) pol_first = l2_policy_first();
   else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_first));
   const uint32_t rows_sa = smem_u32(base);
   const uint32_t wv_sa = rows_sa + L::rows_d * 8;
@@ -1529,40 +1521,18 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       const size_t off = (size_t)r * ld + c0;
       const uint32_t dst = own_sa + (uint32_t)(sl * NOP * W + lane * C) * 8;
       int q = 0;
-      if constexpr (SH) {
-        // the own row of T_k is also gathered by its neighbours: no hint
-        if constexpr (EXPL || MODE == MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.X + off);
-        if constexpr (!FIRST) cp_async_cols_hint<C>(dst + (q++) * W * 8, p.Xprev + off, pol_first);
-        if constexpr (MODE != MODE_DBL) cp_async_cols_hint<C>(dst + (q++) * W * 8, p.Z + off, pol_first);
-      } else {
-        if constexpr (EXPL || MODE == MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.X + off);
-        if constexpr (!FIRST) cp_async_cols<C>(dst + (q++) * W * 8, p.Xprev + off);
-        if constexpr (MODE != MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.Z + off);
-      }
+      // the own row of T_k is also gathered by its neighbours: no hint
+      if constexpr (EXPL || MODE == MODE_DBL) cp_async_cols<C>(dst + (q++) * W * 8, p.X + off);
+      if constexpr (!FIRST) cp_async_cols_hint<C>(dst + (q++) * W * 8, p.Xprev + off, pol_first);
+      if constexpr (MODE != MODE_DBL) cp_async_cols_hint<C>(dst + (q++) * W * 8, p.Z + off, pol_first);
     }
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(obar + sl))
                  : "memory");
   };
-  auto col_slot = [&](int w) {
-    return col_sa + (uint32_t)((w % (HOT ? 4 : 2 * D)) * WAVE * 4);
-  };
-  auto wv_slot = [&](int w) { return wv_sa + (uint32_t)((w % (HOT ? 2 : D)) * WAVE * 8); };
-  int posw = 0;  // HOT: this lane's neighbour's row position in the wave being consumed
-  // HOT: weights of wave w (its col ids have landed)
-  auto issue_weight = [&](int w) {
-    const int e = w * WAVE + lane;
-    if (lane < WAVE && e < nnz) {
-      int jl;
-      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jl) : "r"(col_slot(w) + lane * 4));
-      cp_async_8(wv_slot(w) + lane * 8, p.dinv + jl);
-    }
-  };
+  auto col_slot = [&](int w) { return col_sa + (uint32_t)((w % (2 * D)) * WAVE * 4); };
   auto issue_col = [&](int w) {
     const int e = w * WAVE + lane;
-    if (lane < WAVE && e < nnz) {
-      if constexpr (SH) cp_async_4_first(col_slot(w) + lane * 4, p.col + K0 + e, pol_first);
-      else cp_async_4(col_slot(w) + lane * 4, p.col + K0 + e);
-    }
+    if (lane < WAVE && e < nnz) cp_async_4_first(col_slot(w) + lane * 4, p.col + K0 + e, pol_first);
   };
   // wave w: rows by gather4 (lane 0), weights by lanes < cnt; the caller then
   // lets lanes < WAVE arrive (noinc) after also issuing col(w + D)
@@ -1571,25 +1541,6 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     const int cnt = min(WAVE, nnz - w * WAVE);
     const uint32_t ca = col_slot(w);
     const uint32_t bar = smem_u32(wbar + sl);
-    int nh = 0;
-    if constexpr (HOT) {
-      // stable hot-first partition of the wave's row ids, in place
-      int jk = 0;
-      bool hot = false;
-      if (lane < cnt) {
-        double wk;
-        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jk) : "r"(ca + lane * 4));
-        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(wk) : "r"(wv_slot(w) + lane * 8));
-        hot = wk <= p.hot_dinv_g4;
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, hot);
-      nh = __popc(m);
-      const int below = __popc(m & ((1u << lane) - 1u));
-      posw = hot ? below : nh + lane - below;
-      __syncwarp();
-      if (lane < cnt) asm volatile("st.shared.b32 [%0], %1;" ::"r"(ca + posw * 4), "r"(jk) : "memory");
-      __syncwarp();
-    }
     if (elect_one()) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads of the slot
       int j[WAVE];
@@ -1607,35 +1558,22 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
                    "r"((uint32_t)WAVE * rbytes)
                    : "memory");
       const uint32_t dst = rows_sa + sl * (uint32_t)(L::slot_d * 8);
-      if constexpr (HOT) {
-        // groups with a hot row: no hint; all-cold groups: evict_first
+      // gather-ordered twin: rows are sorted hottest-first, so whole groups
+      // are cold (all four ids >= hot_rows) without any reordering
 #pragma unroll
-        for (int q = 0; q < WAVE / 4; ++q) {
-          if (4 * q >= nh)
-            tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
-                             j[4 * q + 2], j[4 * q + 3], bar, pol_first);
-          else
-            tma_gather4(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
-                        j[4 * q + 2], j[4 * q + 3], bar);
-        }
-      } else {
-        // gather-ordered twin: rows are sorted hottest-first, so whole groups
-        // are cold (all four ids >= hot_rows) without any reordering
-#pragma unroll
-        for (int q = 0; q < WAVE / 4; ++q) {
-          const bool cold = p.hot_rows > 0 && j[4 * q] >= p.hot_rows &&
-                            j[4 * q + 1] >= p.hot_rows && j[4 * q + 2] >= p.hot_rows &&
-                            j[4 * q + 3] >= p.hot_rows;
-          if (cold)
-            tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
-                             j[4 * q + 2], j[4 * q + 3], bar, pol_first);
-          else
-            tma_gather4(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
-                        j[4 * q + 2], j[4 * q + 3], bar);
-        }
+      for (int q = 0; q < WAVE / 4; ++q) {
+        const bool cold = p.hot_rows > 0 && j[4 * q] >= p.hot_rows &&
+                          j[4 * q + 1] >= p.hot_rows && j[4 * q + 2] >= p.hot_rows &&
+                          j[4 * q + 3] >= p.hot_rows;
+        if (cold)
+          tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
+                           j[4 * q + 2], j[4 * q + 3], bar, pol_first);
+        else
+          tma_gather4(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
+                      j[4 * q + 2], j[4 * q + 3], bar);
       }
     }
-    if (!HOT && lane < cnt) {
+    if (lane < cnt) {
       const uint32_t wd = wv_sa + (sl * WAVE + lane) * 8;
       if constexpr (EXPL) {
         cp_async_8(wd, p.vals + K0 + w * WAVE + lane);
@@ -1653,36 +1591,17 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
                    : "memory");
   };
 
-  if constexpr (HOT) {
-    // cols two waves and weights one wave ahead of the rows
-    issue_col(0);
-    issue_col(1);
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
-    issue_weight(0);
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
 #pragma unroll
-    for (int r = 0; r < R; ++r) issue_own(r0 + r);
-    if (nw > 0) {
-      issue_wave(0);
-      issue_weight(1);
-      issue_col(2);
-      arrive_wave(0);
-    }
-  } else {
+  for (int w = 0; w < 2 * D; ++w) issue_col(w);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
 #pragma unroll
-    for (int w = 0; w < 2 * D; ++w) issue_col(w);
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
+  for (int r = 0; r < R; ++r) issue_own(r0 + r);
 #pragma unroll
-    for (int r = 0; r < R; ++r) issue_own(r0 + r);
-#pragma unroll
-    for (int w = 0; w < D; ++w) {
-      if (w < nw) {
-        issue_wave(w);
-        arrive_wave(w);
-      }
+  for (int w = 0; w < D; ++w) {
+    if (w < nw) {
+      issue_wave(w);
+      arrive_wave(w);
     }
   }
 
@@ -1708,8 +1627,8 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       if constexpr (!FIRST) lds_cols<C>(a + (q++) * W * 8, pv);
       if constexpr (MODE != MODE_DBL) lds_cols<C>(a + (q++) * W * 8, zv);
     }
-    bulk_finish_row<C, MODE, EXPL, FIRST, SH>(p, r, active, c0, acc, xo, pv, zv, s1, s2,
-                                              pol_first);
+    bulk_finish_row<C, MODE, EXPL, FIRST, true>(p, r, active, c0, acc, xo, pv, zv, s1, s2,
+                                                pol_first);
     issue_own(r + R);
   };
   auto advance = [&](int64_t kk) {
@@ -1734,15 +1653,10 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     const int e0 = w * WAVE;
     const int cnt = min(WAVE, nnz - e0);
     const uint32_t slot = rows_sa + sl * (uint32_t)(L::slot_d * 8) + my_col;
-    const uint32_t wslot = HOT ? wv_slot(w) : wv_sa + sl * WAVE * 8;
+    const uint32_t wslot = wv_sa + sl * WAVE * 8;
     auto add_h = [&](int k, double h) {
       double v[C];
-      if constexpr (HOT) {
-        const int pk = __shfl_sync(0xffffffffu, posw, k);
-        lds_cols<C>(slot + pk * rbytes, v);
-      } else {
-        lds_cols<C>(slot + k * rbytes, v);
-      }
+      lds_cols<C>(slot + k * rbytes, v);
 #pragma unroll
       for (int c = 0; c < C; ++c)
         acc[c] = __dadd_rn(acc[c], __dmul_rn(h, v[c]));
@@ -1782,14 +1696,8 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     }
     __syncwarp();  // the whole warp is done with the slot and its weights
     if (w + D < nw) {
-      if constexpr (HOT) {
-        issue_wave(w + 1);
-        issue_weight(w + 2);
-        issue_col(w + 3);
-      } else {
-        issue_wave(w + D);
-        issue_col(w + 2 * D);
-      }
+      issue_wave(w + D);
+      issue_col(w + 2 * D);
       arrive_wave(w + D);
     }
   }
@@ -1803,7 +1711,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
   }
 }
 
-template <int C, int MODE, bool EXPL, bool FIRST, bool HOT>
+template <int C, int MODE, bool EXPL, bool FIRST>
 __global__ void __launch_bounds__(KPM_G4_THREADS, G4Tune<C>::minb)
 kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
   using L = G4<C, MODE, EXPL, FIRST>;
@@ -1834,10 +1742,10 @@ kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
       const int64_t t = li / p.n_chunks;
       const int chunk = p.chunk_order[li - t * p.n_chunks];
       if (p.ntiles > 1)
-        light_g4<C, MODE, EXPL, FIRST, HOT>(p, &tm, chunk, p.col0 + t * kTileW, kTileW, base,
+        light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0 + t * kTileW, kTileW, base,
                                             ophase, wphase);
       else
-        light_g4<C, MODE, EXPL, FIRST, HOT>(p, &tm, chunk, p.col0, p.tw, base, ophase, wphase);
+        light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0, p.tw, base, ophase, wphase);
     }
     trace_item(p, item, t0);
   }
@@ -2061,10 +1969,10 @@ static cudaError_t launch_lean_k(const kpm_run *r, const StepParams &p, cudaStre
   return cudaGetLastError();
 }
 
-template <int C, int MODE, bool EXPL, bool FIRST, bool HOT = false>
+template <int C, int MODE, bool EXPL, bool FIRST>
 static cudaError_t launch_g4_k(const kpm_run *r, const StepParams &p, const CUtensorMap &tm,
                                cudaStream_t st) {
-  void (*kern)(StepParams, CUtensorMap) = kpm_step_g4_kernel<C, MODE, EXPL, FIRST, HOT>;
+  void (*kern)(StepParams, CUtensorMap) = kpm_step_g4_kernel<C, MODE, EXPL, FIRST>;
   const int threads = KPM_G4_THREADS;  // warps are independent; CTA size sets smem granularity
   const size_t smem = (size_t)(threads / 32) * G4<C, MODE, EXPL, FIRST>::warp_d * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2092,12 +2000,6 @@ static cudaError_t launch_g4(const kpm_run *r, const StepParams &p, bool expl, b
                              const CUtensorMap &tm, cudaStream_t st) {
   if (expl && first) return launch_g4_k<C, MODE, true, true>(r, p, tm, st);
   if (expl) return launch_g4_k<C, MODE, true, false>(r, p, tm, st);
-  if constexpr (C <= 2 && G4Tune<C>::d == 1) {
-    if (p.g4hot && p.hot_dinv_g4 > 0.0) {
-      if (first) return launch_g4_k<C, MODE, false, true, true>(r, p, tm, st);
-      return launch_g4_k<C, MODE, false, false, true>(r, p, tm, st);
-    }
-  }
   if (first) return launch_g4_k<C, MODE, false, true>(r, p, tm, st);
   return launch_g4_k<C, MODE, false, false>(r, p, tm, st);
 }
@@ -2276,8 +2178,6 @@ static StepParams base_params(const kpm_run *r) {
     if (const char *e = getenv("KPM_HOT_DEGREE")) hot_deg = atof(e);
     if (hot_deg > 0) p.hot_dinv = 1.0 / sqrt(hot_deg);
   }
-  // hot rows of the gather4 path (hot-ordered waves): same rule over the
-  // gathered segment (64-column tiles for the 4-column layouts)
   // gather-ordered twin: the hottest rows (lowest new ids) stay unhinted, every
   // other gather is evict_first (profiles/r02_ncu_summary.md: flat between 100k and 400k rows)
   p.perm = g->perm;
@@ -2286,29 +2186,6 @@ static StepParams base_params(const kpm_run *r) {
     p.hot_rows = 250000;
     if (const char *e = getenv("KPM_HOT_ROWS")) p.hot_rows = atoi(e);
     if (p.hot_rows > g->n) p.hot_rows = (int)g->n;
-  }
-  p.hot_dinv_g4 = -1.0;
-  {
-    double hot_bytes = 64.0 * 1024 * 1024;
-    if (const char *e = getenv("KPM_HOT_MB_G4")) hot_bytes = atof(e) * 1024 * 1024;
-    const bool tiled = r->cpl == 4 && r->ld > kTileW;
-    const int64_t seg = tiled ? kTileW : r->ld;
-    // default (measured, profiles/r01_g4_hot_ab.log): on for the 64-column
-    // tiles when one tile's gathered block is > 200x the L2 (C5: 34 GB, DRAM
-    // -9.5%, step -2.7%); off below that, where plain LRU already keeps the
-    // popular rows and the ordering only costs instructions (C3: +2.6%), and
-    // for the 1-column layout (C3/C5 P=32: +4%)
-    p.g4hot = tiled && 8.0 * (double)seg * (double)g->n > 200.0 * (double)g->ctx->l2_bytes;
-    if (const char *e = getenv("KPM_G4_HOT")) p.g4hot = atoi(e);
-    if (g->perm) p.g4hot = 0;  // the twin's rows are already hot-first
-    const double budget = hot_bytes / (8.0 * (double)seg);
-    double rows = 0.0, hot_deg = 0.0;
-    for (int b = kDegBuckets - 1; b >= 0; --b) {
-      rows += (double)g->deg_hist[b];
-      if (rows > budget) break;
-      hot_deg = deg_bucket_lo(b);
-    }
-    if (hot_deg > 0) p.hot_dinv_g4 = 1.0 / sqrt(hot_deg);
   }
   return p;
 }

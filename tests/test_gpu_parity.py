@@ -509,8 +509,6 @@ def test_filtered_probes_stay_on_device(golden, kpm_ctx):
 # oracle's restated recurrence (the reference's _row order, no FMA).
 _PATHS = {
     "tiles": {},  # default: gather4, 4-column layouts as 64-column passes
-    # hot-ordered gather4 waves, a hot set small enough that waves mix hot and cold rows
-    "hot": {"KPM_G4_HOT": "1", "KPM_HOT_MB_G4": "0.02"},
     "tiles-unfused": {"KPM_FUSE_TILES": "0"},
     "g4": {"KPM_G4": "2", "KPM_TILE": "0"},
     "lean": {"KPM_G4": "0"},

@@ -19,7 +19,6 @@ pytestmark = pytest.mark.gpu
 
 _PATHS = {
     "tiles": {},
-    "hot": {"KPM_G4_HOT": "1", "KPM_HOT_MB_G4": "0.5"},
     "tiles-unfused": {"KPM_FUSE_TILES": "0"},
     "g4": {"KPM_G4": "2", "KPM_TILE": "0"},
     "lean": {"KPM_G4": "0"},
@@ -51,6 +50,28 @@ def rmat16(oracle):
     rp, ci = oracle.csr_from_edges(1 << scale, u, v)
     data = oracle.normadj_values(rp, ci, oracle.dinv_of(rp))
     return scale, ef, seed, rp, ci, data
+
+
+@pytest.mark.parametrize("P", [32, 64, 128])
+def test_twin_runs_repeat_bitwise(oracle, kpm_ctx, monkeypatch, rmat16, P):
+    """The gather-ordered twin (KPM_REORDER=1, a hot set small enough that
+    gather4 groups mix hinted and unhinted copies): repeated runs are bitwise
+    equal to each other and within rounding of the oracle."""
+    scale, ef, seed, rp, ci, data = rmat16
+    for k in _KEYS:
+        monkeypatch.delenv(k, raising=False)
+    monkeypatch.setenv("KPM_REORDER", "1")
+    monkeypatch.setenv("KPM_HOT_ROWS", "500")
+    monkeypatch.setenv("KPM_HEAVY_DEGREE", "3000")
+    dev = kp.DeviceGraph.rmat(scale, ef, seed)
+    probes = kp.make_probes(dev.n, P, "rademacher", seed=P)
+    want = oracle.c_recurrence_block(rp, ci, data, probes.columns, 4, threads=8)
+    for mode in (_lib.MODE_DOS_DOUBLING, _lib.MODE_LDOS):
+        first = _block(dev, probes, mode, 4, kpm_ctx)
+        assert np.max(np.abs(first - want)) <= 1e-13 * np.max(np.abs(want))
+        for rep in range(5):
+            assert np.array_equal(_block(dev, probes, mode, 4, kpm_ctx), first), (P, mode, rep)
+    dev.free()
 
 
 @pytest.mark.parametrize("path", sorted(_PATHS))

@@ -13,9 +13,6 @@ for tool in memcheck racecheck synccheck; do
   echo "== $tool (hub pipeline, KPM_HEAVY_DEGREE=48)" >> $log
   KPM_HEAVY_DEGREE=48 timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 python tools/r2/sanitize_paths.py g4 bulk register >> $log 2>&1
   echo "rc=$?" >> $log
-  echo "== $tool (hot-ordered waves)" >> $log
-  KPM_G4_HOT=1 KPM_HOT_MB_G4=0.02 timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 python tools/r2/sanitize_paths.py g4 >> $log 2>&1
-  echo "rc=$?" >> $log
 done
 # work-item trace of one C5 step (load balance / tail)
 for spec in "c5 128" "c5 32" "c3 128"; do
