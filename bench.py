@@ -66,7 +66,8 @@ CONFIGS = {
 METRIC = "KPM nnz*probes*moments/sec (G/s) and achieved HBM GB/s"
 UNIT = "G nnz*probe*moment/s"
 KERNEL_SOURCES = ("paper_1905_09758_b200/csrc/kpm_step.cu",
-                  "paper_1905_09758_b200/csrc/kpm_internal.cuh")
+                  "paper_1905_09758_b200/csrc/kpm_internal.cuh",
+                  "paper_1905_09758_b200/csrc/kpm_graph.cu")  # the schedule / twin shape the traffic
 
 
 def _code_only(src: str) -> str:

@@ -270,7 +270,14 @@ int finish_graph(kpm_graph *g) {
   }
 
   // capped row costs -> prefix (n+1) ; heavy-row flags
+  // A row goes to the hub path (column slices on dedicated warps) only when one
+  // warp walking it would set the span of the step: the slices gather 128-byte
+  // pieces through cp.async and cost ~4x the light path per nonzero (work-item
+  // traces, profiles/r02_ncu_summary.md section 6), so the bar is the degree at
+  // which a single light row takes about half a step: nnz / 2048 (C3: 254k ->
+  // only the 406k-degree row; C5: 1.03M), never below kHeavyDegree.  Graph-only.
   g->heavy_threshold = kHeavyDegree;
+  if (g->nnz / 2048 > g->heavy_threshold) g->heavy_threshold = g->nnz / 2048;
   if (const char *e = getenv("KPM_HEAVY_DEGREE")) {  // tests force the hub path
     long long v = atoll(e);
     if (v > 0) g->heavy_threshold = v;

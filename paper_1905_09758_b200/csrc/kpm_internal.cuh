@@ -136,7 +136,8 @@ kpm_graph *graph_relabelled(kpm_graph *g);  // kpm_graph.cu; NULL when unavailab
 
 #define KPM_MAX_PARTS 16
 
-// degree from which a row is a "heavy" (hub) row (graph-only constant)
+// lowest degree from which a row can be a "heavy" (hub) row; finish_graph raises
+// the bar to nnz / 2048 on large graphs (graph-only)
 static constexpr int64_t kHeavyDegree = 65536;
 
 struct kpm_run {

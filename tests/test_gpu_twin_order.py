@@ -123,3 +123,41 @@ def test_explicit_graphs_keep_the_reference_order(golden, kpm_ctx, twin):
     assert np.array_equal(_d2h(ptr, (z.shape[0], ld), kpm_ctx)[:, : z.shape[1]],
                           golden["lap60/T3"])
     run.free()
+
+
+def test_zero_mass_node_and_raw_rows_in_caller_numbering(kpm_ctx, twin):
+    """kpm.py:145-147 on the twin: the reported node is the CALLER's id, and
+    the raw per-node sums of that node are zero at that row."""
+    g = kp.preferential_attachment(400, 3, seed=5)   # ids and degree ranks differ
+    sop = kp.scaled_operator_for(g, "normalized-adjacency")
+    z = np.random.default_rng(1).standard_normal((g.n, 3))
+    node = 321
+    z[node] = 0.0
+    zp = kp.ProbeMatrix(g.n, 3, "gaussian", 1, columns=z)
+    with pytest.raises(ValueError, match=f"zero probe mass at node {node}"):
+        kp.pdos_moments(sop, zp, 6)
+    raw = kp.pdos_moments(sop, zp, 6, normalized=False)
+    assert np.all(raw.values[node] == 0.0)
+    assert np.count_nonzero(np.all(raw.values == 0.0, axis=1)) == 1
+
+
+def test_device_filtered_probes_on_the_twin(golden, kpm_ctx, monkeypatch):
+    """Motif-filtered probes stay in HBM (device block) and enter a twin run
+    through the row permutation: moments equal the reference-order run's to
+    rounding, and equal those of the same block uploaded from the host."""
+    n = int(golden["motif/n"])
+    g = kp.GraphCSR(n=n, row_ptr=golden["motif/row_ptr"], col_idx=golden["motif/col_idx"],
+                    weights=np.ones(golden["motif/col_idx"].size), is_weighted=False)
+    insts = kp.detect_motifs(g, seed=3)
+    sop = kp.scaled_operator_for(g, "normalized-adjacency")
+    monkeypatch.setenv("KPM_REORDER", "0")
+    fd0, adj = kp.filter_probes(kp.make_probes(n, 16, "rademacher", seed=3), insts)
+    want = kp.dos_moments(sop, fd0, 60, effective_dim=n - adj.deflated_dim)
+    monkeypatch.setenv("KPM_REORDER", "1")
+    fd, _ = kp.filter_probes(kp.make_probes(n, 16, "rademacher", seed=3), insts)
+    assert fd.device_block is not None and fd._columns is None
+    got = kp.dos_moments(sop, fd, 60, effective_dim=n - adj.deflated_dim)
+    host = kp.ProbeMatrix(n, 16, "rademacher", 3, columns=fd0.columns)
+    got_h = kp.dos_moments(sop, host, 60, effective_dim=n - adj.deflated_dim)
+    assert np.array_equal(got.values, got_h.values)
+    assert _normwise(got.values, want.values) <= 1e-12
