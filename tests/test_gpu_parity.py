@@ -529,11 +529,12 @@ def test_light_paths_bitexact(oracle, kpm_ctx, monkeypatch, path, P, hubs):
     if hubs:
         monkeypatch.setenv("KPM_HEAVY_DEGREE", "40")
     g = kp.preferential_attachment(3000, 3, seed=P)
-    # 70 isolated vertices inserted at id 1500 and 30 appended: runs of empty rows
+    # 70 isolated vertices inserted at id 1500 and 300 appended: runs of empty rows, and
+    # whole chunks of them (the streamed empty-chunk path)
     ins = lambda v: v + 70 * (v >= 1500)
     deg = np.diff(g.row_ptr)
-    deg = np.concatenate([deg[:1500], np.zeros(70, np.int64), deg[1500:], np.zeros(30, np.int64)])
-    n = g.n + 100
+    deg = np.concatenate([deg[:1500], np.zeros(70, np.int64), deg[1500:], np.zeros(300, np.int64)])
+    n = g.n + 370
     rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
     ci = ins(g.col_idx.astype(np.int64))
     z = oracle.make_probes(n, P, "rademacher", seed=P + 1)
