@@ -521,6 +521,24 @@ __global__ void relab_keys(const int64_t *__restrict__ row_ptr, const int32_t *_
 
 // The twin of an implicit, unpartitioned graph (see kpm_graph::relab); NULL
 // when it cannot be built (explicit values, partitions, out of memory).
+// Twin rows are degree-descending: thread e finds the first row whose degree is
+// <= kDinvSteps - 1 - e (n when none) and that degree's d^-1/2.
+__global__ void dinv_steps_kernel(const int64_t *__restrict__ row_ptr,
+                                  const double *__restrict__ dinv, int64_t n,
+                                  int32_t *__restrict__ step_id, double *__restrict__ step_val) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= kDinvSteps) return;
+  const int64_t d = kDinvSteps - 1 - e;
+  int64_t lo = 0, hi = n;  // first row in [0, n] with degree <= d
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (row_ptr[mid + 1] - row_ptr[mid] <= d) hi = mid;
+    else lo = mid + 1;
+  }
+  step_id[e] = lo < n ? (int32_t)lo : 0x7fffffff;
+  step_val[e] = lo < n ? dinv[lo] : 0.0;
+}
+
 kpm_graph *graph_relabelled(kpm_graph *g) {
   if (g->relab_state != 0) return g->relab;
   g->relab_state = -1;
@@ -567,6 +585,23 @@ kpm_graph *graph_relabelled(kpm_graph *g) {
   t->perm = perm;
   t->iperm = iperm;
   t->relab_state = -1;  // a twin has no twin
+  if (cudaMalloc(&t->dstep_id, sizeof(int32_t) * kDinvSteps) == cudaSuccess &&
+      cudaMalloc(&t->dstep_val, sizeof(double) * kDinvSteps) == cudaSuccess) {
+    dinv_steps_kernel<<<(kDinvSteps + 127) / 128, 128, 0, st>>>(t->row_ptr, t->dinv, n,
+                                                                 t->dstep_id, t->dstep_val);
+    if (cudaMemcpyAsync(&t->dstep_h, t->dstep_id, sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(t->dstep_id); cudaFree(t->dstep_val);
+      t->dstep_id = nullptr; t->dstep_val = nullptr;
+      t->dstep_h = 0x7fffffff;
+    }
+  } else {
+    cudaGetLastError();
+    cudaFree(t->dstep_id);
+    t->dstep_id = nullptr;
+  }
   g->relab = t;
   g->relab_state = 1;
   return t;
@@ -890,6 +925,8 @@ void kpm_graph_free(kpm_graph *g) {
   cudaFree(g->dinv_all);
   cudaFree(g->perm);
   cudaFree(g->iperm);
+  cudaFree(g->dstep_id);
+  cudaFree(g->dstep_val);
   if (g->relab) kpm_graph_free(g->relab);
   delete g;
 }

@@ -128,7 +128,17 @@ struct kpm_graph {
   kpm_graph *relab = nullptr;
   int relab_state = 0;  // 0 not tried, 1 built, -1 unavailable
   int32_t *perm = nullptr, *iperm = nullptr;
+  // twin only: d^-1/2 as a step function of the (degree-ranked) id.  Ids
+  // >= dstep_id[0] have degree < kDinvSteps; dstep_id[e] is the first id with
+  // degree <= kDinvSteps - 1 - e (ascending in e), dstep_val[e] that degree's
+  // dinv (copied from dinv, bit-identical).  The step kernel looks the cold
+  // ids' dinv_j up in this table (shared memory) instead of gathering 8 bytes
+  // per nonzero from the n-entry array (a DRAM sector each at R-MAT scale).
+  int32_t *dstep_id = nullptr;
+  double *dstep_val = nullptr;
+  int32_t dstep_h = 0x7fffffff;  // = dstep_id[0]
 };
+static constexpr int kDinvSteps = 512;
 
 namespace kpm {
 kpm_graph *graph_relabelled(kpm_graph *g);  // kpm_graph.cu; NULL when unavailable

@@ -84,6 +84,12 @@ struct StepParams {
   int fuse_tiles;          // run all 64-column tiles of a step as one launch
   int hot_rows;            // gather-ordered twin: gathered ids < hot_rows are hot (L2 policy)
   const int32_t *perm;     // gather-ordered twin: perm[row] = the caller's row id (else NULL)
+  // gather-ordered twin: d^-1/2 of ids >= dstep_h from the degree-step table
+  // (kpm_graph::dstep_id / dstep_val, staged in shared memory) instead of an
+  // 8-byte gather per nonzero; dstep_h = INT32_MAX: no table
+  const int32_t *dstep_id;
+  const double *dstep_val;
+  int dstep_h;
   int64_t hub_off;         // dynamic smem (doubles) of warp 0's hub ring (kpm_step_kernel)
   unsigned long long *trace;  // KPM_TRACE: per work item (start ns, end ns, smid<<32|warp)
 };
@@ -1458,7 +1464,8 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm,
 template <int C, int MODE, bool EXPL, bool FIRST>
 __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap *tm, int chunk,
                                          const int64_t col0, const int64_t tw, double *base,
-                                         uint32_t &ophase, uint32_t &wphase) {
+                                         uint32_t &ophase, uint32_t &wphase,
+                                         const uint32_t dtab_sa) {
   using L = G4<C, MODE, EXPL, FIRST>;
   constexpr int D = L::D, R = L::R, W = L::W, NOP = L::NOP, WAVE = L::WAVE;
   const int lane = threadIdx.x & 31;
@@ -1580,7 +1587,23 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       } else {
         int jl;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jl) : "r"(ca + lane * 4));
-        cp_async_8(wd, p.dinv + jl);
+        if (jl >= p.dstep_h) {
+          // twin: ids are degree ranks, so dinv is a step function of the id;
+          // largest e with dstep_id[e] <= jl (dstep_id[0] = dstep_h), then the
+          // same double the array holds
+          uint32_t e = 0;
+#pragma unroll
+          for (int s = kDinvSteps / 2; s > 0; s >>= 1) {
+            int t;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(t) : "r"(dtab_sa + (e + s) * 4));
+            if (t <= jl) e += s;
+          }
+          double dv;
+          asm volatile("ld.shared.f64 %0, [%1];" : "=d"(dv) : "r"(dtab_sa + kDinvSteps * 4 + e * 8));
+          asm volatile("st.shared.f64 [%0], %1;" ::"r"(wd), "d"(dv) : "memory");
+        } else {
+          cp_async_8(wd, p.dinv + jl);
+        }
       }
     }
   };
@@ -1650,6 +1673,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     const uint32_t sl = (uint32_t)(w % D);
     mbar_wait(wbar + sl, (wphase >> sl) & 1u);
     wphase ^= 1u << sl;
+    if (p.dstep_h != 0x7fffffff) __syncwarp();  // table weights were plain shared stores
     const int e0 = w * WAVE;
     const int cnt = min(WAVE, nnz - e0);
     const uint32_t slot = rows_sa + sl * (uint32_t)(L::slot_d * 8) + my_col;
@@ -1716,6 +1740,18 @@ __global__ void __launch_bounds__(KPM_G4_THREADS, G4Tune<C>::minb)
 kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
   using L = G4<C, MODE, EXPL, FIRST>;
   extern __shared__ __align__(128) double sg4[];
+  // degree-step table of the twin: [kDinvSteps] int32 first ids, then the doubles
+  __shared__ __align__(8) unsigned char s_dtab[kDinvSteps * 12];
+  if (p.dstep_h != 0x7fffffff) {
+    int32_t *did = reinterpret_cast<int32_t *>(s_dtab);
+    double *dval = reinterpret_cast<double *>(s_dtab + kDinvSteps * 4);
+    for (int e = threadIdx.x; e < kDinvSteps; e += blockDim.x) {
+      did[e] = p.dstep_id[e];
+      dval[e] = p.dstep_val[e];
+    }
+    __syncthreads();
+  }
+  const uint32_t dtab_sa = smem_u32(s_dtab);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   double *base = sg4 + (size_t)warp * L::warp_d;
@@ -1743,9 +1779,10 @@ kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
       const int chunk = p.chunk_order[li - t * p.n_chunks];
       if (p.ntiles > 1)
         light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0 + t * kTileW, kTileW, base,
-                                            ophase, wphase);
+                                            ophase, wphase, dtab_sa);
       else
-        light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0, p.tw, base, ophase, wphase);
+        light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0, p.tw, base, ophase, wphase,
+                                       dtab_sa);
     }
     trace_item(p, item, t0);
   }
@@ -2181,6 +2218,15 @@ static StepParams base_params(const kpm_run *r) {
   // gather-ordered twin: the hottest rows (lowest new ids) stay unhinted, every
   // other gather is evict_first (profiles/r02_ncu_summary.md: flat between 100k and 400k rows)
   p.perm = g->perm;
+  p.dstep_id = g->dstep_id;
+  p.dstep_val = g->dstep_val;
+  p.dstep_h = 0x7fffffff;
+  if (g->dstep_id && g->dstep_val) {
+    p.dstep_h = g->dstep_h;
+    if (const char *e = getenv("KPM_DINV_TABLE")) {
+      if (atoi(e) == 0) p.dstep_h = 0x7fffffff;
+    }
+  }
   p.hot_rows = 0;
   if (g->perm) {
     p.hot_rows = 250000;

@@ -161,3 +161,40 @@ def test_device_filtered_probes_on_the_twin(golden, kpm_ctx, monkeypatch):
     got_h = kp.dos_moments(sop, host, 60, effective_dim=n - adj.deflated_dim)
     assert np.array_equal(got.values, got_h.values)
     assert _normwise(got.values, want.values) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", [(13, 16, 3), (15, 24, 5), (9, 2, 1)])
+@pytest.mark.parametrize("k", [32, 64, 128, 20])
+def test_dinv_step_table_is_bitwise_the_gathered_dinv(kpm_ctx, monkeypatch, shape, k):
+    """On the twin the ids are degree ranks, so d^-1/2 is a step function of the
+    id: ids of degree < 512 take dinv_j from a shared-memory table of
+    (first id, dinv) steps instead of an 8-byte gather per nonzero
+    (kpm_graph::dstep_id).  The table holds the doubles of the dinv array, so
+    every T_k block is bitwise the one of the gathering kernel
+    (KPM_DINV_TABLE=0) -- graphs with rows on both sides of the cut, only
+    below it, isolated vertices, and every gather4 layout."""
+    scale, ef, seed = shape
+    monkeypatch.setenv("KPM_REORDER", "1")
+    dev = kp.DeviceGraph.rmat(scale, ef, seed)
+    deg = np.diff(dev.export()[0])
+    assert deg.min() == 0
+    assert (deg.max() >= 512) == (scale >= 13)
+    probes = kp.make_probes(dev.n, k, "rademacher", seed=7)
+    out = {}
+    for table in ("1", "0"):
+        monkeypatch.setenv("KPM_DINV_TABLE", table)
+        for mode in (_lib.MODE_DOS_DOUBLING, _lib.MODE_LDOS):
+            run = Run(dev, k, mode, 12)
+            try:
+                run.set_probes(probes)
+                run.advance(5)
+                blk, ld, idx = run.block()
+                out[table, mode] = (_d2h(blk, (dev.n, ld), kpm_ctx).copy(), idx)
+            finally:
+                run.free()
+    for mode in (_lib.MODE_DOS_DOUBLING, _lib.MODE_LDOS):
+        a, b = out["1", mode], out["0", mode]
+        assert a[1] == b[1] == 5
+        assert np.abs(a[0]).max() > 0
+        assert np.array_equal(a[0], b[0])
+    dev.free()
