@@ -1404,6 +1404,9 @@ __global__ void __launch_bounds__(256, KPM_LEAN_MINB) kpm_step_lean_kernel(const
 #ifndef KPM_G4_OWN
 #define KPM_G4_OWN 4
 #endif
+#ifndef KPM_G4_SEG
+#define KPM_G4_SEG 0
+#endif
 #ifndef KPM_G4_THREADS
 #define KPM_G4_THREADS 256
 #endif
@@ -1548,6 +1551,13 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
     const int cnt = min(WAVE, nnz - w * WAVE);
     const uint32_t ca = col_slot(w);
     const uint32_t bar = smem_u32(wbar + sl);
+    // this lane's neighbour id (weights below); one ballot gives the elected
+    // lane every group's "all four ids cold" test (ids past a chunk's last
+    // nonzero vote hot: their group just goes unhinted)
+    int jl = 0;
+    if (lane < cnt) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jl) : "r"(ca + lane * 4));
+    const uint32_t cold_mask =
+        __ballot_sync(0xffffffffu, p.hot_rows > 0 && lane < cnt && jl >= p.hot_rows);
     if (elect_one()) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads of the slot
       int j[WAVE];
@@ -1569,9 +1579,7 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       // are cold (all four ids >= hot_rows) without any reordering
 #pragma unroll
       for (int q = 0; q < WAVE / 4; ++q) {
-        const bool cold = p.hot_rows > 0 && j[4 * q] >= p.hot_rows &&
-                          j[4 * q + 1] >= p.hot_rows && j[4 * q + 2] >= p.hot_rows &&
-                          j[4 * q + 3] >= p.hot_rows;
+        const bool cold = ((cold_mask >> (4 * q)) & 0xFu) == 0xFu;
         if (cold)
           tma_gather4_hint(dst + 4 * q * rbytes, tm, (int)col0, j[4 * q], j[4 * q + 1],
                            j[4 * q + 2], j[4 * q + 3], bar, pol_first);
@@ -1585,8 +1593,6 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       if constexpr (EXPL) {
         cp_async_8(wd, p.vals + K0 + w * WAVE + lane);
       } else {
-        int jl;
-        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(jl) : "r"(ca + lane * 4));
         if (jl >= p.dstep_h) {
           // twin: ids are degree ranks, so dinv is a step function of the id;
           // largest e with dstep_id[e] <= jl (dstep_id[0] = dstep_h), then the
@@ -1713,10 +1719,21 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       }
       advance(e0 + WAVE);
     } else {
+#if KPM_G4_SEG
+      // row by row: the current row's nonzeros inside this wave without a
+      // row-end test per nonzero (advance() left rend > e0 + k)
+      int k = 0;
+      while (k < cnt) {
+        const int kend = (int)min((int64_t)cnt, rend - e0);
+        for (; k < kend; ++k) add_one(k);
+        advance(e0 + k);
+      }
+#else
       for (int k = 0; k < cnt; ++k) {
         add_one(k);
         advance(e0 + k + 1);
       }
+#endif
     }
     __syncwarp();  // the whole warp is done with the slot and its weights
     if (w + D < nw) {
@@ -1777,9 +1794,13 @@ kpm_step_g4_kernel(const StepParams p, const __grid_constant__ CUtensorMap tm) {
       const int64_t li = (int64_t)item - p.n_heavy_tasks;
       const int64_t t = li / p.n_chunks;
       const int chunk = p.chunk_order[li - t * p.n_chunks];
-      if (p.ntiles > 1)
+      // constant tile widths give the consumer immediate shared-memory offsets
+      if (C == 2 && p.ntiles > 1)
         light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0 + t * kTileW, kTileW, base,
                                             ophase, wphase, dtab_sa);
+      else if (p.tw == 32 * C)
+        light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0, 32 * C, base, ophase, wphase,
+                                       dtab_sa);
       else
         light_g4<C, MODE, EXPL, FIRST>(p, &tm, chunk, p.col0, p.tw, base, ophase, wphase,
                                        dtab_sa);
