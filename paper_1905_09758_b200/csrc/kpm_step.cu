@@ -1404,9 +1404,6 @@ __global__ void __launch_bounds__(256, KPM_LEAN_MINB) kpm_step_lean_kernel(const
 #ifndef KPM_G4_OWN
 #define KPM_G4_OWN 4
 #endif
-#ifndef KPM_G4_SEG
-#define KPM_G4_SEG 0
-#endif
 #ifndef KPM_G4_THREADS
 #define KPM_G4_THREADS 256
 #endif
@@ -1719,21 +1716,14 @@ __device__ __forceinline__ void light_g4(const StepParams &p, const CUtensorMap 
       }
       advance(e0 + WAVE);
     } else {
-#if KPM_G4_SEG
       // row by row: the current row's nonzeros inside this wave without a
       // row-end test per nonzero (advance() left rend > e0 + k)
       int k = 0;
       while (k < cnt) {
-        const int kend = (int)min((int64_t)cnt, rend - e0);
+        const int kend = max(k + 1, (int)min((int64_t)cnt, rend - e0));
         for (; k < kend; ++k) add_one(k);
         advance(e0 + k);
       }
-#else
-      for (int k = 0; k < cnt; ++k) {
-        add_one(k);
-        advance(e0 + k + 1);
-      }
-#endif
     }
     __syncwarp();  // the whole warp is done with the slot and its weights
     if (w + D < nw) {
