@@ -29,6 +29,22 @@ def test_traffic_entries_match_current_kernel():
         assert "ncu" in e["source"]
 
 
+def test_traffic_lies_between_the_byte_models_and_read_peak_is_recorded():
+    """The measured DRAM bytes of a launch sit between the compulsory bytes and
+    the per-nonzero gather model, and the read-gather peak that bench.py prints
+    beside the copy peak (frac_of_read_peak) comes with its provenance."""
+    with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+        rec = json.load(f)
+    sizes = {"c5": (1 << 26, 2103834148), "c3": (1 << 24, 520768910)}
+    for key, e in rec["entries"].items():
+        cfg, p = key.split("/P")
+        n, nnz = sizes[cfg]
+        assert bench.bytes_compulsory(n, nnz, int(p)) < e["dram_bytes"] < bench.bytes_model(n, nnz, int(p))
+    gbs, src = bench.read_gather_peak()
+    assert 6000.0 < gbs < 8000.0 and "gather_bw" in src
+    assert os.path.exists(os.path.join(REPO, "profiles", "r02_gather_roofline.log"))
+
+
 def test_kernel_hash_ignores_comments():
     a = bench._code_only("int x = 1;  // note\n/* block\n comment */ int y;\n")
     b = bench._code_only("int x = 1;\nint   y;")
